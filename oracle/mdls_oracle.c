@@ -1,0 +1,790 @@
+/*
+ * oracle/mdls_oracle.c -- CPU ORACLE FOR THE MULTIPLE-DOUBLE LEAST-SQUARES PATH.
+ *
+ *   *** TEST INFRASTRUCTURE ONLY. ***  Only tests/, __graft_entry__.smoke() and
+ *   bench.py's cpu_baseline / --impl reference legs may load this library.  The
+ *   product (paper_2110_08375_b200/, libmdls.so) never links, imports or calls it,
+ *   and this file shares no code, header, table or constant with the CUDA path.
+ *
+ * What it computes (PAPER.md = arXiv 2110.08375, cited as P:<line>):
+ *   - multiple double numbers: unevaluated sums of m doubles, m = 2 (dd), 4 (qd),
+ *     8 (od).  Arithmetic is the paper's named families: QDlib for dd
+ *      and CAMPARY's generated qd/od code (P:152-156,
+ *     P:615-625).  The paper prints no algorithm, only their Table 1 operation
+ *     counts; the exact variants below are the readings of DESIGN.md
+ *     ("md arithmetic readings"), which reproduce every octo double cell of
+ *     Table 1 exactly (tests/test_oracle_counts.py pins that).
+ *   - blocked Householder QR reaches the same (Q, R) as the textbook
+ *     unblocked Householder QR in exact arithmetic; this oracle IS that textbook
+ *     computation (Golub & Van Loan Alg. 5.1.1 house + Alg. 5.2.1 QR),
+ *     carried out in md arithmetic, with Q accumulated backward.
+ *   - tiled back substitution reaches the same x as plain back
+ *     substitution; this oracle is plain row back substitution.
+ *   - least squares: A = QR, R x = Q^T b.
+ *
+ * Storage: an md matrix is m plain double matrices, most significant
+ * first.  Plane l of an R x C operand starts at ptr + l*ld*C, column-major with
+ * leading dimension ld.  Vectors are m planes of length n (stride n).
+ *
+ * Build: gcc -O2 -ffp-contract=off -fno-fast-math (no FMA contraction: the
+ * error-free transformations below depend on every +,-,* being rounded once).
+ * With -DMDLS_ORACLE_COUNT every base-double +,-,*,/ is tallied (Table 1 pins).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define MAXM 8
+
+/* ------------------------------------------------------------------------- */
+/* base double operations, optionally counted                                 */
+/* ------------------------------------------------------------------------- */
+#ifdef MDLS_ORACLE_COUNT
+static uint64_t g_cnt[4]; /* additions, subtractions, multiplications, divisions */
+static inline double ADD(double a, double b) { g_cnt[0]++; return a + b; }
+static inline double SUB(double a, double b) { g_cnt[1]++; return a - b; }
+static inline double MUL(double a, double b) { g_cnt[2]++; return a * b; }
+static inline double DIV(double a, double b) { g_cnt[3]++; return a / b; }
+/* negation of one limb: Table 1 tallies it as a subtraction (md readings) */
+static inline double NEG(double a) { g_cnt[1]++; return -a; }
+void oracle_count_reset(void) { memset(g_cnt, 0, sizeof(g_cnt)); }
+void oracle_count_get(uint64_t *out) { memcpy(out, g_cnt, sizeof(g_cnt)); }
+int oracle_is_counting(void) { return 1; }
+#else
+static inline double ADD(double a, double b) { return a + b; }
+static inline double SUB(double a, double b) { return a - b; }
+static inline double MUL(double a, double b) { return a * b; }
+static inline double DIV(double a, double b) { return a / b; }
+static inline double NEG(double a) { return -a; }
+void oracle_count_reset(void) {}
+void oracle_count_get(uint64_t *out) { memset(out, 0, 4 * sizeof(uint64_t)); }
+int oracle_is_counting(void) { return 0; }
+#endif
+
+/* ------------------------------------------------------------------------- */
+/* error-free transformations                                                 */
+/* ------------------------------------------------------------------------- */
+
+/* two_sum (Knuth): s = fl(a+b), e = a+b-s exactly.  2 additions, 4 subtractions. */
+static void two_sum(double a, double b, double *s, double *e) {
+  double ss = ADD(a, b);
+  double bb = SUB(ss, a);
+  *e = ADD(SUB(a, SUB(ss, bb)), SUB(b, bb));
+  *s = ss;
+}
+
+/* quick_two_sum / Fast2Sum (Dekker), valid when |a| >= |b|: 1 addition, 2 subtractions. */
+static void quick_two_sum(double a, double b, double *s, double *e) {
+  double ss = ADD(a, b);
+  *e = SUB(b, SUB(ss, a));
+  *s = ss;
+}
+
+/* Veltkamp split as in QDlib: a = hi + lo, each half fits in 26 bits. */
+static void split(double a, double *hi, double *lo) {
+  const double SPLITTER = 134217729.0;               /* 2^27 + 1 */
+  const double SPLIT_THRESH = 6.69692879491417e+299; /* 2^996 */
+  if (a > SPLIT_THRESH || a < -SPLIT_THRESH) {
+    double as = a * 3.7252902984619140625e-09; /* 2^-28 */
+    double t = MUL(SPLITTER, as);
+    double h = SUB(t, SUB(t, as));
+    double l = SUB(as, h);
+    *hi = h * 268435456.0; /* 2^28 */
+    *lo = l * 268435456.0;
+  } else {
+    double t = MUL(SPLITTER, a);
+    *hi = SUB(t, SUB(t, a));
+    *lo = SUB(a, *hi);
+  }
+}
+
+/* two_prod (Dekker, no FMA): p = fl(a*b), e = a*b-p exactly.
+ * 7 multiplications, 3 additions, 7 subtractions (the tally Table 1 implies). */
+static void two_prod(double a, double b, double *p, double *e) {
+  double ah, al, bh, bl;
+  double pp = MUL(a, b);
+  split(a, &ah, &al);
+  split(b, &bh, &bl);
+  *e = ADD(ADD(ADD(SUB(MUL(ah, bh), pp), MUL(ah, bl)), MUL(al, bh)), MUL(al, bl));
+  *p = pp;
+}
+
+/* exported for the EFT exactness pins */
+void oracle_two_sum(double a, double b, double *out) { two_sum(a, b, &out[0], &out[1]); }
+void oracle_quick_two_sum(double a, double b, double *out) { quick_two_sum(a, b, &out[0], &out[1]); }
+void oracle_two_prod(double a, double b, double *out) { two_prod(a, b, &out[0], &out[1]); }
+void oracle_split(double a, double *out) { split(a, &out[0], &out[1]); }
+
+/* ------------------------------------------------------------------------- */
+/* double double (QDlib)                                           */
+/* ------------------------------------------------------------------------- */
+
+/* QDlib dd_real::ieee_add. 8 additions, 12 subtractions (Table 1 dd add row). */
+static void dd_add(const double *a, const double *b, double *c) {
+  double s1, s2, t1, t2;
+  two_sum(a[0], b[0], &s1, &s2);
+  two_sum(a[1], b[1], &t1, &t2);
+  s2 = ADD(s2, t1);
+  quick_two_sum(s1, s2, &s1, &s2);
+  s2 = ADD(s2, t2);
+  quick_two_sum(s1, s2, &c[0], &c[1]);
+}
+
+/* QDlib dd * dd: two_prod of the leading limbs plus the two cross products. */
+static void dd_mul(const double *a, const double *b, double *c) {
+  double p1, p2;
+  two_prod(a[0], b[0], &p1, &p2);
+  p2 = ADD(p2, ADD(MUL(a[0], b[1]), MUL(a[1], b[0])));
+  quick_two_sum(p1, p2, &c[0], &c[1]);
+}
+
+/* QDlib dd * double. */
+static void dd_mul_d(const double *a, double b, double *c) {
+  double p1, p2;
+  two_prod(a[0], b, &p1, &p2);
+  p2 = ADD(p2, MUL(a[1], b));
+  quick_two_sum(p1, p2, &c[0], &c[1]);
+}
+
+/* QDlib dd + double. */
+static void dd_add_d(const double *a, double b, double *c) {
+  double s1, s2;
+  two_sum(a[0], b, &s1, &s2);
+  s2 = ADD(s2, a[1]);
+  quick_two_sum(s1, s2, &c[0], &c[1]);
+}
+
+static void dd_sub(const double *a, const double *b, double *c) {
+  double nb[2] = {NEG(b[0]), NEG(b[1])};
+  dd_add(a, nb, c);
+}
+
+/* QDlib dd_real::accurate_div: three quotient digits q1, q2, q3. */
+static void dd_div(const double *a, const double *b, double *c) {
+  double q1, q2, q3, r[2], t[2];
+  q1 = DIV(a[0], b[0]);
+  dd_mul_d(b, q1, t);
+  dd_sub(a, t, r); /* r = a - q1*b */
+  q2 = DIV(r[0], b[0]);
+  dd_mul_d(b, q2, t);
+  dd_sub(r, t, r); /* r -= q2*b */
+  q3 = DIV(r[0], b[0]);
+  quick_two_sum(q1, q2, &q1, &q2);
+  double q[2] = {q1, q2};
+  dd_add_d(q, q3, c);
+}
+
+/* QDlib dd sqrt: one Newton correction of the double reciprocal square root
+ * (P:633-635): x = 1/sqrt(a0); ax = a0*x; c = ax + (a - ax^2)_0 * (x/2). */
+static void dd_sqrt(const double *a, double *c) {
+  if (a[0] == 0.0) { c[0] = c[1] = 0.0; return; }
+  double x = DIV(1.0, sqrt(a[0]));
+  double ax = MUL(a[0], x);
+  double sq[2], d[2];
+  two_prod(ax, ax, &sq[0], &sq[1]);
+  dd_sub(a, sq, d);
+  two_sum(ax, MUL(d[0], MUL(x, 0.5)), &c[0], &c[1]);
+}
+
+/* ------------------------------------------------------------------------- */
+/* quad double and octo double (CAMPARY "fast" family)             */
+/* ------------------------------------------------------------------------- */
+
+/* Renormalisation of m+1 terms to m limbs (CAMPARY fast_renorm2L<m+1,m>):
+ * 2m-1 Fast2Sums.  Level 1 is a bottom-up Fast2Sum sweep over f[0..m]; level 2
+ * is a top-down sweep over its first m outputs that emits a limb whenever the
+ * Fast2Sum error is nonzero, then zero-pads.  (Reading: DESIGN.md.) */
+static void renorm(int m, const double *f, double *r) {
+  double g[MAXM + 1];
+  double s = f[m];
+  for (int i = m - 1; i >= 0; --i) quick_two_sum(f[i], s, &s, &g[i + 1]);
+  g[0] = s;
+  double eps = g[0];
+  int j = 0;
+  for (int i = 1; i <= m - 1; ++i) {
+    double rr, e;
+    quick_two_sum(eps, g[i], &rr, &e);
+    if (e != 0.0) {
+      r[j++] = rr;
+      eps = e;
+    } else {
+      eps = rr;
+    }
+  }
+  r[j++] = eps;
+  for (; j < m; ++j) r[j] = 0.0;
+}
+
+/* CAMPARY baileyAdd_fast<m,m,m>: position sums from the least significant
+ * upward; each error is carried by two_sums through the less significant
+ * positions and its remainder added into the tail term f[m]. */
+static void mdg_add(int m, const double *a, const double *b, double *c) {
+  double f[MAXM + 1], e;
+  f[m] = 0.0;
+  for (int i = m - 1; i >= 0; --i) {
+    two_sum(a[i], b[i], &f[i], &e);
+    for (int j = i + 1; j < m; ++j) two_sum(f[j], e, &f[j], &e);
+    f[m] = ADD(f[m], e);
+  }
+  renorm(m, f, c);
+}
+
+/* carry an error term x through f[n+1..m-1] and into the tail f[m] */
+static void carry(int m, int n, double *f, double x) {
+  for (int j = n + 1; j < m; ++j) two_sum(f[j], x, &f[j], &x);
+  f[m] = ADD(f[m], x);
+}
+
+/* CAMPARY baileyMul_fast<m,la,lb> for la, lb in {1, m}, m output limbs:
+ *   f[m] = sum of the plain products a_i*b_j with i+j = m;
+ *   for levels n = m-1 .. 0: every two_prod a_i*b_{n-i} (i ascending) is summed
+ *   into f[n] by two_sum (the first is assigned), its product error and then
+ *   the sum error are carried through f[n+1..m-1] into f[m];
+ *   then renorm(f[0..m]). */
+static void mdg_mul_gen(int m, int la, const double *a, int lb, const double *b, double *c) {
+  double f[MAXM + 1];
+  int first = 1;
+  f[m] = 0.0;
+  for (int i = 0; i < la; ++i) {
+    int j = m - i;
+    if (j < 0 || j >= lb) continue;
+    double p = MUL(a[i], b[j]);
+    if (first) { f[m] = p; first = 0; } else f[m] = ADD(f[m], p);
+  }
+  for (int n = m - 1; n >= 0; --n) {
+    int have = 0;
+    for (int i = 0; i <= n; ++i) {
+      int j = n - i;
+      if (i >= la || j >= lb) continue;
+      double p, pe, e;
+      two_prod(a[i], b[j], &p, &pe);
+      if (!have) {
+        f[n] = p;
+        have = 1;
+        carry(m, n, f, pe);
+      } else {
+        two_sum(f[n], p, &f[n], &e);
+        carry(m, n, f, pe);
+        carry(m, n, f, e);
+      }
+    }
+    if (!have) f[n] = 0.0;
+  }
+  renorm(m, f, c);
+}
+
+static void mdg_mul(int m, const double *a, const double *b, double *c) { mdg_mul_gen(m, m, a, m, b, c); }
+
+/* long division: q0 = a0/b0; for i = 1..m: r -= q_{i-1}*b (md x double, the
+ * subtraction an addition of the negated limbs); q_i = r0/b0; renorm(q0..qm). */
+static void mdg_div(int m, const double *a, const double *b, double *c) {
+  double q[MAXM + 1], r[MAXM], t[MAXM], qb[1];
+  memcpy(r, a, sizeof(double) * m);
+  q[0] = DIV(a[0], b[0]);
+  for (int i = 1; i <= m; ++i) {
+    qb[0] = q[i - 1];
+    mdg_mul_gen(m, m, b, 1, qb, t);
+    for (int k = 0; k < m; ++k) t[k] = NEG(t[k]);
+    mdg_add(m, r, t, r);
+    q[i] = DIV(r[0], b[0]);
+  }
+  renorm(m, q, c);
+}
+
+/* QDlib-style square root extended to m limbs: Newton on the
+ * reciprocal square root, y <- y + (1/2 - (a/2) y^2) y, from y0 = 1/sqrt(a0),
+ * ceil(log2 m)+1 times; result a*y. */
+static void mdg_sqrt(int m, const double *a, double *c) {
+  if (a[0] == 0.0) { memset(c, 0, sizeof(double) * m); return; }
+  int iters = (m == 4) ? 3 : 4;
+  double y[MAXM] = {0}, h[MAXM], t[MAXM], half[MAXM] = {0};
+  y[0] = DIV(1.0, sqrt(a[0]));
+  half[0] = 0.5;
+  for (int k = 0; k < m; ++k) h[k] = a[k] * 0.5; /* exact scaling by a power of two */
+  for (int it = 0; it < iters; ++it) {
+    mdg_mul(m, y, y, t);
+    mdg_mul(m, h, t, t);
+    for (int k = 0; k < m; ++k) t[k] = NEG(t[k]);
+    mdg_add(m, half, t, t);
+    mdg_mul(m, t, y, t);
+    mdg_add(m, y, t, y);
+  }
+  mdg_mul(m, a, y, c);
+}
+
+/* ------------------------------------------------------------------------- */
+/* precision dispatch                                                         */
+/* ------------------------------------------------------------------------- */
+static void md_add(int m, const double *a, const double *b, double *c) {
+  if (m == 2) dd_add(a, b, c); else mdg_add(m, a, b, c);
+}
+static void md_mul(int m, const double *a, const double *b, double *c) {
+  if (m == 2) dd_mul(a, b, c); else mdg_mul(m, a, b, c);
+}
+static void md_div(int m, const double *a, const double *b, double *c) {
+  if (m == 2) dd_div(a, b, c); else mdg_div(m, a, b, c);
+}
+static void md_sqrt(int m, const double *a, double *c) {
+  if (m == 2) dd_sqrt(a, c); else mdg_sqrt(m, a, c);
+}
+static void md_neg(int m, const double *a, double *c) {
+  for (int k = 0; k < m; ++k) c[k] = NEG(a[k]);
+}
+static void md_sub(int m, const double *a, const double *b, double *c) {
+  double nb[MAXM];
+  md_neg(m, b, nb);
+  md_add(m, a, nb, c);
+}
+static void md_zero(int m, double *c) { memset(c, 0, sizeof(double) * m); }
+static void md_set_d(int m, double d, double *c) { md_zero(m, c); c[0] = d; }
+static void md_copy(int m, const double *a, double *c) { memcpy(c, a, sizeof(double) * m); }
+/* sign of a renormalised expansion is the sign of its leading limb */
+static double md_lead(const double *a) { return a[0]; }
+static void md_abs(int m, const double *a, double *c) {
+  if (a[0] < 0.0) md_neg(m, a, c); else md_copy(m, a, c);
+}
+/* a < b  <=>  lead(a - b) < 0 */
+static int md_lt(int m, const double *a, const double *b) {
+  double d[MAXM];
+  md_sub(m, a, b, d);
+  return d[0] < 0.0;
+}
+
+/* vectorised single-operation entry point (op: 0 add, 1 sub, 2 mul, 3 div, 4 sqrt) */
+int oracle_md_op(int op, int m, int64_t n, const double *a, const double *b, double *c) {
+  if (m != 2 && m != 4 && m != 8) return -2;
+  for (int64_t i = 0; i < n; ++i) {
+    double x[MAXM], y[MAXM], z[MAXM];
+    for (int k = 0; k < m; ++k) {
+      x[k] = a[k * n + i];
+      y[k] = b ? b[k * n + i] : 0.0;
+    }
+    switch (op) {
+      case 0: md_add(m, x, y, z); break;
+      case 1: md_sub(m, x, y, z); break;
+      case 2: md_mul(m, x, y, z); break;
+      case 3: md_div(m, x, y, z); break;
+      case 4: md_sqrt(m, x, z); break;
+      default: return -1;
+    }
+    for (int k = 0; k < m; ++k) c[k * n + i] = z[k];
+  }
+  return 0;
+}
+/* renormalisation of an (m+1)-term array, for the renorm pins */
+int oracle_renorm(int m, const double *f, double *r) {
+  if (m != 2 && m != 4 && m != 8) return -2;
+  renorm(m, f, r);
+  return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* limb-planar element access                                                 */
+/* ------------------------------------------------------------------------- */
+typedef struct {
+  double *p;
+  int64_t ld, cols;
+  int m;
+} mat_t;
+
+static inline void get(const mat_t *A, int64_t i, int64_t j, double *x) {
+  for (int k = 0; k < A->m; ++k) x[k] = A->p[k * A->ld * A->cols + j * A->ld + i];
+}
+static inline void put(const mat_t *A, int64_t i, int64_t j, const double *x) {
+  for (int k = 0; k < A->m; ++k) A->p[k * A->ld * A->cols + j * A->ld + i] = x[k];
+}
+
+static void set_threads(int nthreads) {
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#else
+  (void)nthreads;
+#endif
+}
+
+/* ------------------------------------------------------------------------- */
+/* Householder vector: Golub & Van Loan (3rd ed.) Algorithm 5.1.1  */
+/* x = x[0..n-1] (md, contiguous m-limb records).  On return v[0] = 1, beta,  */
+/* and mu = the first entry of P x (= ||x||_2 when sigma != 0, else x1).      */
+/* ------------------------------------------------------------------------- */
+static void house(int m, int64_t n, const double *x, double *v, double *beta, double *mu) {
+  double sigma[MAXM], t[MAXM], x1[MAXM];
+  md_zero(m, sigma);
+  for (int64_t i = 1; i < n; ++i) { /* sigma = x(2:n)^T x(2:n), ascending */
+    md_mul(m, &x[i * m], &x[i * m], t);
+    md_add(m, sigma, t, sigma);
+  }
+  md_copy(m, &x[0], x1);
+  md_set_d(m, 1.0, &v[0]);
+  for (int64_t i = 1; i < n; ++i) md_copy(m, &x[i * m], &v[i * m]);
+  if (md_lead(sigma) == 0.0) {
+    md_zero(m, beta);
+    md_copy(m, x1, mu);
+    return;
+  }
+  double x1sq[MAXM], mu_[MAXM], v1[MAXM], v1sq[MAXM], num[MAXM], den[MAXM];
+  md_mul(m, x1, x1, x1sq);
+  md_add(m, x1sq, sigma, t);
+  md_sqrt(m, t, mu_); /* mu = sqrt(x1^2 + sigma) */
+  if (md_lead(x1) <= 0.0) {
+    md_sub(m, x1, mu_, v1); /* v1 = x1 - mu */
+  } else {
+    double ns[MAXM];
+    md_neg(m, sigma, ns);
+    md_add(m, x1, mu_, t);
+    md_div(m, ns, t, v1); /* v1 = -sigma / (x1 + mu) */
+  }
+  md_mul(m, v1, v1, v1sq);
+  double two[MAXM];
+  md_set_d(m, 2.0, two);
+  md_mul(m, two, v1sq, num);
+  md_add(m, sigma, v1sq, den);
+  md_div(m, num, den, beta); /* beta = 2 v1^2 / (sigma + v1^2) */
+  for (int64_t i = 1; i < n; ++i) md_div(m, &v[i * m], v1, &v[i * m]); /* v = v / v1 */
+  md_copy(m, mu_, mu);
+}
+
+int oracle_house(int m, int64_t n, const double *x_planes, double *v_planes, double *beta, double *mu) {
+  if (m != 2 && m != 4 && m != 8) return -2;
+  double *x = malloc(sizeof(double) * m * n), *v = malloc(sizeof(double) * m * n);
+  for (int64_t i = 0; i < n; ++i)
+    for (int k = 0; k < m; ++k) x[i * m + k] = x_planes[k * n + i];
+  house(m, n, x, v, beta, mu);
+  for (int64_t i = 0; i < n; ++i)
+    for (int k = 0; k < m; ++k) v_planes[k * n + i] = v[i * m + k];
+  free(x);
+  free(v);
+  return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* unblocked Householder QR (GVL Alg. 5.2.1)                                  */
+/* A (M x K, ld >= M): on exit R in the upper triangle (R_jj = mu, the        */
+/* sub-diagonal part of column j holds v_j(2:), v_j(1) = 1 implicit);          */
+/* beta: m planes of K.  Every dot product accumulates from 0 ascending.       */
+/* ------------------------------------------------------------------------- */
+int oracle_qr(int m, int64_t M, int64_t K, double *Ap, int64_t lda, double *beta_p, int nthreads) {
+  if (m != 2 && m != 4 && m != 8) return -2;
+  if (M < K || K < 0 || lda < M) return -1;
+  set_threads(nthreads);
+  mat_t A = {Ap, lda, K, m};
+  double *x = malloc(sizeof(double) * m * (M + 1));
+  double *v = malloc(sizeof(double) * m * (M + 1));
+  for (int64_t j = 0; j < K; ++j) {
+    int64_t n = M - j;
+    for (int64_t i = 0; i < n; ++i) get(&A, j + i, j, &x[i * m]);
+    double beta[MAXM], mu[MAXM];
+    house(m, n, x, v, beta, mu);
+    /* apply P = I - beta v v^T to the columns c > j (independent: threaded) */
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t c = j + 1; c < K; ++c) {
+      double s[MAXM], t[MAXM], a[MAXM], w[MAXM];
+      md_zero(m, s);
+      for (int64_t i = 0; i < n; ++i) { /* s = v . A(j:M, c) */
+        get(&A, j + i, c, a);
+        md_mul(m, &v[i * m], a, t);
+        md_add(m, s, t, s);
+      }
+      md_mul(m, beta, s, w); /* w = beta * s */
+      for (int64_t i = 0; i < n; ++i) { /* A(j:M, c) -= w v */
+        get(&A, j + i, c, a);
+        md_mul(m, w, &v[i * m], t);
+        md_sub(m, a, t, a);
+        put(&A, j + i, c, a);
+      }
+    }
+    put(&A, j, j, mu);
+    for (int64_t i = 1; i < n; ++i) put(&A, j + i, j, &v[i * m]);
+    for (int k = 0; k < m; ++k) beta_p[k * K + j] = beta[k];
+  }
+  free(x);
+  free(v);
+  return 0;
+}
+
+/* load v_j (full length M-j, v_j(1) = 1) from the factored A */
+static void load_v(const mat_t *A, int64_t M, int64_t j, double *v) {
+  int m = A->m;
+  md_set_d(m, 1.0, &v[0]);
+  for (int64_t i = 1; i < M - j; ++i) get(A, j + i, j, &v[i * m]);
+}
+
+/* Q = H_1 H_2 ... H_K, accumulated backward: Q = I; for j = K..1:
+ * Q(j:M, c) -= beta_j (v_j . Q(j:M, c)) v_j for the columns c >= j. */
+int oracle_form_q(int m, int64_t M, int64_t K, const double *Ap, int64_t lda, const double *beta_p, double *Qp,
+                  int64_t ldq, int nthreads) {
+  if (m != 2 && m != 4 && m != 8) return -2;
+  if (M < K || ldq < M || lda < M) return -1;
+  set_threads(nthreads);
+  mat_t A = {(double *)Ap, lda, K, m};
+  mat_t Q = {Qp, ldq, M, m};
+  for (int k = 0; k < m; ++k) memset(Qp + (int64_t)k * ldq * M, 0, sizeof(double) * ldq * M);
+  for (int64_t i = 0; i < M; ++i) Qp[i * ldq + i] = 1.0;
+  double *v = malloc(sizeof(double) * m * (M + 1));
+  for (int64_t j = K - 1; j >= 0; --j) {
+    int64_t n = M - j;
+    load_v(&A, M, j, v);
+    double beta[MAXM];
+    for (int k = 0; k < m; ++k) beta[k] = beta_p[k * K + j];
+#pragma omp parallel for schedule(dynamic, 4)
+    for (int64_t c = j; c < M; ++c) {
+      double s[MAXM], t[MAXM], a[MAXM], w[MAXM];
+      md_zero(m, s);
+      for (int64_t i = 0; i < n; ++i) {
+        get(&Q, j + i, c, a);
+        md_mul(m, &v[i * m], a, t);
+        md_add(m, s, t, s);
+      }
+      md_mul(m, beta, s, w);
+      for (int64_t i = 0; i < n; ++i) {
+        get(&Q, j + i, c, a);
+        md_mul(m, w, &v[i * m], t);
+        md_sub(m, a, t, a);
+        put(&Q, j + i, c, a);
+      }
+    }
+  }
+  free(v);
+  return 0;
+}
+
+/* y = Q^T b by applying the reflectors: y = b; for j = 1..K:
+ * y(j:M) -= beta_j (v_j . y(j:M)) v_j. */
+int oracle_apply_qt(int m, int64_t M, int64_t K, const double *Ap, int64_t lda, const double *beta_p,
+                    const double *b, double *y) {
+  if (m != 2 && m != 4 && m != 8) return -2;
+  mat_t A = {(double *)Ap, lda, K, m};
+  mat_t Y = {y, M, 1, m};
+  if (y != b) memcpy(y, b, sizeof(double) * m * M);
+  double *v = malloc(sizeof(double) * m * (M + 1));
+  for (int64_t j = 0; j < K; ++j) {
+    int64_t n = M - j;
+    load_v(&A, M, j, v);
+    double beta[MAXM], s[MAXM], t[MAXM], a[MAXM], w[MAXM];
+    for (int k = 0; k < m; ++k) beta[k] = beta_p[k * K + j];
+    md_zero(m, s);
+    for (int64_t i = 0; i < n; ++i) {
+      get(&Y, j + i, 0, a);
+      md_mul(m, &v[i * m], a, t);
+      md_add(m, s, t, s);
+    }
+    md_mul(m, beta, s, w);
+    for (int64_t i = 0; i < n; ++i) {
+      get(&Y, j + i, 0, a);
+      md_mul(m, w, &v[i * m], t);
+      md_sub(m, a, t, a);
+      put(&Y, j + i, 0, a);
+    }
+  }
+  free(v);
+  return 0;
+}
+
+/* y = Q^T b with an explicit Q (y_c = sum_i Q(i,c) b_i, ascending i). */
+int oracle_qt_b_explicit(int m, int64_t M, const double *Qp, int64_t ldq, const double *b, double *y,
+                         int nthreads) {
+  if (m != 2 && m != 4 && m != 8) return -2;
+  set_threads(nthreads);
+  mat_t Q = {(double *)Qp, ldq, M, m};
+  mat_t B = {(double *)b, M, 1, m};
+  double *out = malloc(sizeof(double) * m * M);
+#pragma omp parallel for schedule(static)
+  for (int64_t c = 0; c < M; ++c) {
+    double s[MAXM], t[MAXM], q[MAXM], bb[MAXM];
+    md_zero(m, s);
+    for (int64_t i = 0; i < M; ++i) {
+      get(&Q, i, c, q);
+      get(&B, i, 0, bb);
+      md_mul(m, q, bb, t);
+      md_add(m, s, t, s);
+    }
+    for (int k = 0; k < m; ++k) out[k * M + c] = s[k];
+  }
+  memcpy(y, out, sizeof(double) * m * M);
+  free(out);
+  return 0;
+}
+
+/* plain back substitution on the leading n x n of R: for i = n..1:
+ * s = y_i; for l = i+1..n: s -= R_il x_l; x_i = s / R_ii.
+ * Returns 0, or i+1 (1-based) for the first zero diagonal met. */
+int oracle_backsub(int m, int64_t n, const double *Rp, int64_t ldr, int64_t rcols, const double *y, int64_t ylen,
+                   double *x) {
+  if (m != 2 && m != 4 && m != 8) return -2;
+  mat_t R = {(double *)Rp, ldr, rcols, m};
+  double *xx = malloc(sizeof(double) * m * (n + 1));
+  int info = 0;
+  for (int64_t i = n - 1; i >= 0; --i) {
+    double s[MAXM], t[MAXM], r[MAXM];
+    for (int k = 0; k < m; ++k) s[k] = y[k * ylen + i];
+    for (int64_t l = i + 1; l < n; ++l) {
+      get(&R, i, l, r);
+      md_mul(m, r, &xx[l * m], t);
+      md_sub(m, s, t, s);
+    }
+    get(&R, i, i, r);
+    if (r[0] == 0.0 && !info) info = (int)(i + 1);
+    md_div(m, s, r, &xx[i * m]);
+  }
+  for (int64_t i = 0; i < n; ++i)
+    for (int k = 0; k < m; ++k) x[k * n + i] = xx[i * m + k];
+  free(xx);
+  return info;
+}
+
+/* ------------------------------------------------------------------------- */
+/* least squares: A = QR (A copied), y = Q^T b (reflectors), R x = y(1:K)      */
+/* ------------------------------------------------------------------------- */
+int oracle_lstsq(int m, int64_t M, int64_t K, const double *Ap, int64_t lda, const double *b, double *x,
+                 double *R_out, double *y_out, int nthreads) {
+  if (m != 2 && m != 4 && m != 8) return -2;
+  double *F = malloc(sizeof(double) * m * M * K);
+  for (int k = 0; k < m; ++k)
+    for (int64_t j = 0; j < K; ++j)
+      memcpy(F + (int64_t)k * M * K + j * M, Ap + (int64_t)k * lda * K + j * lda, sizeof(double) * M);
+  double *beta = malloc(sizeof(double) * m * K);
+  double *y = malloc(sizeof(double) * m * M);
+  int rc = oracle_qr(m, M, K, F, M, beta, nthreads);
+  if (!rc) rc = oracle_apply_qt(m, M, K, F, M, beta, b, y);
+  if (!rc) rc = oracle_backsub(m, K, F, M, K, y, M, x);
+  if (R_out) {
+    for (int k = 0; k < m; ++k)
+      for (int64_t j = 0; j < K; ++j)
+        for (int64_t i = 0; i < M; ++i)
+          R_out[(int64_t)k * M * K + j * M + i] = (i <= j) ? F[(int64_t)k * M * K + j * M + i] : 0.0;
+  }
+  if (y_out) memcpy(y_out, y, sizeof(double) * m * M);
+  free(F);
+  free(beta);
+  free(y);
+  return rc;
+}
+
+/* ------------------------------------------------------------------------- */
+/* invariants (computed in md, returned as the leading limb)                  */
+/* ------------------------------------------------------------------------- */
+
+/* E1 = max |Q^T Q - I| over the columns listed (all when cols == NULL). */
+double oracle_inv_orth(int m, int64_t M, const double *Qp, int64_t ldq, const int64_t *cols, int64_t ncols,
+                       int nthreads) {
+  set_threads(nthreads);
+  mat_t Q = {(double *)Qp, ldq, M, m};
+  int64_t nc = cols ? ncols : M;
+  double worst = 0.0;
+#pragma omp parallel for schedule(dynamic, 1) reduction(max : worst)
+  for (int64_t cc = 0; cc < nc; ++cc) {
+    int64_t c = cols ? cols[cc] : cc;
+    for (int64_t r = 0; r < M; ++r) {
+      double s[MAXM], t[MAXM], a[MAXM], b[MAXM], one[MAXM];
+      md_zero(m, s);
+      for (int64_t i = 0; i < M; ++i) {
+        get(&Q, i, r, a);
+        get(&Q, i, c, b);
+        md_mul(m, a, b, t);
+        md_add(m, s, t, s);
+      }
+      if (r == c) {
+        md_set_d(m, 1.0, one);
+        md_sub(m, s, one, s);
+      }
+      double e = fabs(s[0]);
+      if (e > worst) worst = e;
+    }
+  }
+  return worst;
+}
+
+/* E2 = max |A - Q R| / max |A| over the listed columns (R upper K x K block in an M x K array). */
+double oracle_inv_recon(int m, int64_t M, int64_t K, const double *Ap, int64_t lda, const double *Qp, int64_t ldq,
+                        const double *Rp, int64_t ldr, const int64_t *cols, int64_t ncols, int nthreads) {
+  set_threads(nthreads);
+  mat_t A = {(double *)Ap, lda, K, m}, Q = {(double *)Qp, ldq, M, m}, R = {(double *)Rp, ldr, K, m};
+  int64_t nc = cols ? ncols : K;
+  double worst = 0.0, amax = 0.0;
+  for (int64_t j = 0; j < K; ++j)
+    for (int64_t i = 0; i < M; ++i) {
+      double a = fabs(Ap[j * lda + i]);
+      if (a > amax) amax = a;
+    }
+#pragma omp parallel for schedule(dynamic, 1) reduction(max : worst)
+  for (int64_t cc = 0; cc < nc; ++cc) {
+    int64_t c = cols ? cols[cc] : cc;
+    for (int64_t i = 0; i < M; ++i) {
+      double s[MAXM], t[MAXM], q[MAXM], r[MAXM], a[MAXM];
+      md_zero(m, s);
+      for (int64_t l = 0; l <= c; ++l) {
+        get(&Q, i, l, q);
+        get(&R, l, c, r);
+        md_mul(m, q, r, t);
+        md_add(m, s, t, s);
+      }
+      get(&A, i, c, a);
+      md_sub(m, a, s, s);
+      double e = fabs(s[0]);
+      if (e > worst) worst = e;
+    }
+  }
+  return amax > 0 ? worst / amax : worst;
+}
+
+/* E3 = ||A^T (b - A x)||_inf / (||A||_inf (||A||_inf ||x||_inf + ||b||_inf)). */
+double oracle_inv_normal(int m, int64_t M, int64_t K, const double *Ap, int64_t lda, const double *x,
+                         const double *b, int nthreads) {
+  set_threads(nthreads);
+  mat_t A = {(double *)Ap, lda, K, m};
+  double *r = malloc(sizeof(double) * m * M);
+  double anorm = 0.0, xnorm = 0.0, bnorm = 0.0;
+#pragma omp parallel for schedule(static) reduction(max : anorm)
+  for (int64_t i = 0; i < M; ++i) { /* r = b - A x, and the row sums of |A| */
+    double s[MAXM], t[MAXM], a[MAXM], xx[MAXM];
+    for (int k = 0; k < m; ++k) s[k] = b[k * M + i];
+    double rowsum = 0.0;
+    for (int64_t j = 0; j < K; ++j) {
+      get(&A, i, j, a);
+      for (int k = 0; k < m; ++k) xx[k] = x[k * K + j];
+      md_mul(m, a, xx, t);
+      md_sub(m, s, t, s);
+      rowsum += fabs(a[0]);
+    }
+    for (int k = 0; k < m; ++k) r[k * M + i] = s[k];
+    if (rowsum > anorm) anorm = rowsum;
+  }
+  for (int64_t j = 0; j < K; ++j) xnorm = fmax(xnorm, fabs(x[j]));
+  for (int64_t i = 0; i < M; ++i) bnorm = fmax(bnorm, fabs(b[i]));
+  double worst = 0.0;
+#pragma omp parallel for schedule(static) reduction(max : worst)
+  for (int64_t j = 0; j < K; ++j) { /* A^T r */
+    double s[MAXM], t[MAXM], a[MAXM], rr[MAXM];
+    md_zero(m, s);
+    for (int64_t i = 0; i < M; ++i) {
+      get(&A, i, j, a);
+      for (int k = 0; k < m; ++k) rr[k] = r[k * M + i];
+      md_mul(m, a, rr, t);
+      md_add(m, s, t, s);
+    }
+    double e = fabs(s[0]);
+    if (e > worst) worst = e;
+  }
+  free(r);
+  double den = anorm * (anorm * xnorm + bnorm);
+  return den > 0 ? worst / den : worst;
+}
+
+/* runtime self-check of round-to-nearest-even without reassociation:
+ * two_sum(2^53, 1) must give (2^53, 1). */
+int oracle_selfcheck(void) {
+  double s, e;
+  two_sum(9007199254740992.0, 1.0, &s, &e);
+  return (s == 9007199254740992.0 && e == 1.0) ? 0 : 1;
+}
+
+/* silence unused-function warnings for helpers kept for completeness */
+void oracle_unused_(void) {
+  double a[MAXM] = {0}, b[MAXM] = {0};
+  (void)md_lt(2, a, b);
+  md_abs(2, a, b);
+}
