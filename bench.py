@@ -1,0 +1,417 @@
+#!/usr/bin/env python
+"""Benchmark: multiple-double least squares (arXiv 2110.08375) on B200.
+
+One "step" = one least-squares solve through the whole hot path (all SURVEY
+8(a) rows): blocked Householder QR with W/Y accumulation and the trailing
+update, backward Q formation, Q^T b with the explicit Q, tiled back
+substitution (tile inversion + the multiply/update chain) -- the paper's
+Table 11 pipeline.  Default workload = BASELINE config 2:
+double double, 1,024 x 1,024, tile 128.
+
+Metric (BASELINE.json): md QR+backsub double flops/s, i.e. canonical md-op
+counts (mdls_count) weighted with the paper's Table 1 sums
+(P:102-136), divided by device time; reported in GFLOP/s with the fraction of
+the B200 FP64 peak (37.2 TFLOP/s = 148 SMs x 64 DFMA/clk x 2 x 1.965 GHz).
+
+Launch: python bench.py [--gpus N --steps K --warmup W] [--impl reference].
+N > 1 runs under torchrun, one rank per GPU, each rank solving its own
+problem (batch sharding, no collective): weak scaling, max time over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (precision, M, K, nb)
+    "cfg1": ("dd", 64, 64, 8),
+    "cfg2": ("dd", 1024, 1024, 128),
+    "cfg3qd": ("qd", 1024, 1024, 128),
+    "cfg3od": ("od", 1024, 1024, 128),
+}
+METRIC = "md QR+backsub double-flops/s & % FP64 peak at n=1024 dd/qd/od, 1/2/4/8 B200"
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12      # 37.2 (FMA = 2 flops)
+FP64_PIPE_TOPS = 148 * 64 * 1.965e9 / 1e12            # 18.6 FP64-pipe lane ops/s (DADD/DMUL/DFMA each 1)
+# FP64 pipe instructions per md pair (one md mul + one md add) as the kernels implement them
+# (md.cuh: FMA two_prod): dd 9+20, qd 182+85, od 1202+269
+OPS_PER_PAIR = {"dd": 29, "qd": 267, "od": 1471}
+# paper's V100 times for the same least-squares workload (T11): QR + BS kernel ms
+PAPER_V100_MS = {"dd": 451.1 + 4.0, "qd": 3020.6 + 28.0, "od": 11924.5 + 114.5}
+L2_FLUSH_BYTES = 512 << 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg2")
+    ap.add_argument("--no-extra", action="store_true", help="skip the qd/od side measurements")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline")
+    ap.add_argument("--no-graph", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.out = None
+
+    def __enter__(self):
+        try:
+            self.out = open(f"/tmp/mdls_clocks_{os.getpid()}.csv", "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=self.out, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.out:
+            self.out.close()
+
+    def summary(self):
+        try:
+            rows = [l.strip().split(",") for l in open(self.out.name) if l.strip()]
+        except Exception:
+            rows = []
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = sorted(float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit())
+        mx = max(float(r[2]) for r in rows if r[2].strip().replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in rows:
+            for k, name in enumerate(names):
+                if len(r) > 5 + k and "Active" in r[5 + k] and "Not" not in r[5 + k]:
+                    reasons.add(name)
+        loaded = [v for v in sm if v > 0.5 * mx] or sm
+        return {"sm_mhz": loaded[len(loaded) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(rows)}
+
+
+def make_problem(prec, M, K, seed):
+    from paper_2110_08375_b200 import inputs
+
+    return inputs.lstsq_problem(M, K, prec, seed)
+
+
+def ledger_flops(prec, M, K, nb, form_q=True):
+    import paper_2110_08375_b200 as mdls
+
+    c = mdls.counts(prec, 2 if form_q else 4, M, K, nb)
+    return c
+
+
+def gemm_pairs(ledger):
+    """md pairs computed by the md GEMM kernels (WY build, trailing update, Q formation, Q^T b)."""
+    st = ledger["stages"]
+    return sum(st[s]["mul"] for s in ("wy", "trailing", "form_q", "qtb"))
+
+
+def run_ours(args, ws, rank, local):
+    import numpy as np
+    import torch
+
+    import paper_2110_08375_b200 as mdls
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if ws > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if ws == 1:
+            return v
+        import torch.distributed as dist
+
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    prec, M, K, nb = WORKLOADS[args.workload]
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+
+    def measure(prec, M, K, nb, steps, warmup, seed, with_e2e, with_trace, sampler=None):
+        A_h, b_h = make_problem(prec, M, K, seed)
+        A = torch.from_numpy(A_h).to(dev)
+        b = torch.from_numpy(b_h).to(dev)
+        work = torch.empty(mdls.workspace_bytes(prec, 2, M, K, nb), dtype=torch.uint8, device=dev)
+        stream = torch.cuda.current_stream()
+
+        def step():
+            return mdls.lstsq(prec, A, b, nb, form_q=True, work=work)
+
+        for _ in range(warmup):
+            r = step()
+        torch.cuda.synchronize()
+        assert int(r.info.item()) == 0, f"dev_info={int(r.info.item())}"
+        # capture one solve in a CUDA graph (launch-bound inner loops, no host work per step)
+        graph = None
+        n0 = mdls.launch_count()
+        if not args.no_graph:
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                gr = step()
+            per_step_launches = mdls.launch_count() - n0
+            graph.replay()
+            torch.cuda.synchronize()
+        else:
+            step()
+            torch.cuda.synchronize()
+            per_step_launches = mdls.launch_count() - n0
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        barrier()
+        torch.cuda.synchronize()
+        ctx = sampler if sampler is not None else _Null()
+        with ctx:
+            for i in range(steps):
+                flush.fill_(float(i))  # L2 flush between timed steps (untimed)
+                ev[i][0].record(stream)
+                if graph is not None:
+                    graph.replay()
+                else:
+                    step()
+                ev[i][1].record(stream)
+            torch.cuda.synchronize()
+        barrier()
+        ms = [a.elapsed_time(bb) for a, bb in ev]
+        ms_step = max_over_ranks(sum(ms) / steps)
+        out = {"ms_per_step": ms_step, "ms_min": min(ms), "launches_per_step": per_step_launches}
+        if with_trace:  # second pass, traced launch by launch (per-stage and per-family kernel times)
+            mdls.trace_enable(True)
+            for i in range(steps):
+                flush.fill_(float(i))
+                step()
+            torch.cuda.synchronize()
+            mdls.trace_enable(False)
+            tr = mdls.trace_collect()
+            out["trace"] = {k: ({s: v / steps for s, v in d.items()} if isinstance(d, dict) else d / steps)
+                            for k, d in tr.items()}
+        if with_e2e:  # through the public API from pinned host buffers, copies inside the timed region
+            A_p = torch.from_numpy(A_h).pin_memory()
+            b_p = torch.from_numpy(b_h).pin_memory()
+            x_p = torch.empty((A_h.shape[0], K), dtype=torch.float64).pin_memory()
+            A_d = torch.empty_like(A)
+            b_d = torch.empty_like(b)
+            for _ in range(2):
+                A_d.copy_(A_p, non_blocking=True)
+                b_d.copy_(b_p, non_blocking=True)
+                rr = mdls.lstsq(prec, A_d, b_d, nb, form_q=True, work=work)
+                x_p.copy_(rr.x, non_blocking=True)
+            torch.cuda.synchronize()
+            barrier()
+            t0 = torch.cuda.Event(enable_timing=True)
+            t1 = torch.cuda.Event(enable_timing=True)
+            t0.record(stream)
+            for _ in range(steps):
+                A_d.copy_(A_p, non_blocking=True)
+                b_d.copy_(b_p, non_blocking=True)
+                rr = mdls.lstsq(prec, A_d, b_d, nb, form_q=True, work=work)
+                x_p.copy_(rr.x, non_blocking=True)
+            t1.record(stream)
+            torch.cuda.synchronize()
+            barrier()
+            out["e2e_ms"] = max_over_ranks(t0.elapsed_time(t1) / steps)
+            out["h2d"] = A_h.nbytes + b_h.nbytes
+            out["d2h"] = x_p.numel() * 8
+            # parity guard on the e2e result (cheap invariant: finite, dev_info 0)
+            assert int(rr.info.item()) == 0 and bool(np.isfinite(x_p.numpy()).all())
+        return out
+
+    sampler = ClockSampler(local)
+    main = measure(prec, M, K, nb, args.steps, args.warmup, seed=rank, with_e2e=True, with_trace=True,
+                   sampler=sampler)
+    led = ledger_flops(prec, M, K, nb)
+    flops = led["total_flops"]
+    value = ws * flops / (main["ms_per_step"] * 1e-3) / 1e9  # GFLOP/s, whole job
+    e2e_val = ws * flops / (main["e2e_ms"] * 1e-3) / 1e9
+    tr = main["trace"]
+    gemm_ms = tr["family_ms"]["gemm"]
+    pairs = gemm_pairs(led)
+    achieved = pairs * OPS_PER_PAIR[prec] / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
+    res = {
+        "metric": METRIC,
+        "value": round(value, 2),
+        "unit": "GFLOP/s",
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(main["ms_per_step"], 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic",
+        "config": {
+            "workload": f"{prec} least squares {M}x{K}, tile {nb} (QR + W/Y + trailing + Q + Q^T b + tiled BS)",
+            "precision": prec, "M": M, "K": K, "nb": nb,
+            "parallelism": f"batch{ws}" if ws > 1 else "single",
+            "l2": f"flushed between timed steps ({L2_FLUSH_BYTES >> 20} MiB write, untimed)",
+            "graph": not args.no_graph,
+            "flops_per_solve": flops,
+        },
+        "fp64_peak_frac": round(value / ws / (FP64_PEAK_TFLOPS * 1e3), 4),
+        "fp64_peak_tflops": round(FP64_PEAK_TFLOPS, 2),
+        "clocks": sampler.summary(),
+        "e2e": {"value": round(e2e_val, 2), "unit": "GFLOP/s", "h2d_bytes_per_step": main["h2d"],
+                "d2h_bytes_per_step": main["d2h"], "ms_per_step": round(main["e2e_ms"], 4)},
+        "gpu_launches": int(main["launches_per_step"] * args.steps),
+        "roofline": {
+            "kernel": "gemm_kernel (md GEMM: WY build, trailing update, Q formation, Q^T b)",
+            "bound": "alu",
+            "achieved": round(achieved, 3) if achieved else None,
+            "peak": round(FP64_PIPE_TOPS, 2),
+            "unit": "TFLOP/s",
+            "unit_note": "FP64-pipe lane operations (DADD/DMUL/DFMA each 1) per second; peak = 148 SMs x 64 "
+                         "lanes x 1.965 GHz (measured DADD 18.56 T/s, profiles/r01_fp64_peak.txt)",
+            "frac": round(achieved / FP64_PIPE_TOPS, 4) if achieved else None,
+            "traffic": None,
+            "algorithmic_ops_per_step": pairs * OPS_PER_PAIR[prec],
+            "kernel_ms_per_step": round(gemm_ms, 4),
+            "share_of_step": round(gemm_ms / main["ms_per_step"], 4),
+            "measured": "CUDA events around every library launch over a second traced pass of the same steps",
+        },
+        "stages_ms": {k: round(v, 4) for k, v in tr["stages_ms"].items()},
+        "family_ms": {k: round(v, 4) for k, v in tr["family_ms"].items()},
+        "paper_context": {
+            "V100_kernel_ms_T11": PAPER_V100_MS[prec],
+            "speedup_vs_V100_kernel_time": round(PAPER_V100_MS[prec] / main["ms_per_step"], 1),
+            "note": "paper GF rates use its own (~14x larger) tallies; compare time per solve",
+        },
+    }
+    if not args.no_extra and args.workload == "cfg2":
+        extra = {"dd": {"ms_per_solve": round(main["ms_per_step"], 4), "gflops": round(value / ws, 2)}}
+        for p, steps in (("qd", max(2, min(args.steps, 5))), ("od", max(2, min(args.steps, 3)))):
+            r = measure(p, M, K, nb, steps, 1, seed=rank, with_e2e=False, with_trace=False)
+            f = ledger_flops(p, M, K, nb)["total_flops"]
+            extra[p] = {"ms_per_solve": round(r["ms_per_step"], 3),
+                        "gflops": round(f / (r["ms_per_step"] * 1e-3) / 1e9, 2),
+                        "fp64_peak_frac": round(f / (r["ms_per_step"] * 1e-3) / 1e12 / FP64_PEAK_TFLOPS, 4),
+                        "speedup_vs_V100_kernel_time": round(PAPER_V100_MS[p] / r["ms_per_step"], 1)}
+        res["precisions"] = extra
+        res["overhead"] = {
+            "dd_to_qd": round(extra["qd"]["ms_per_solve"] / extra["dd"]["ms_per_solve"], 2),
+            "qd_to_od": round(extra["od"]["ms_per_solve"] / extra["qd"]["ms_per_solve"], 2),
+            "predicted_T1": {"dd_to_qd": 11.7, "qd_to_od": 5.4},
+        }
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        res["cpu_baseline"] = cpu_baseline(prec, M, K, nb)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+def cpu_baseline(prec, M, K, nb, repeats=1):
+    """The oracle (plain C, threads over independent columns) on the host cores."""
+    import oracle
+
+    oracle.build()
+    cores = oracle.default_threads()
+    A, b = make_problem(prec, M, K, 0)
+    t0 = time.perf_counter()
+    for _ in range(repeats):
+        oracle.lstsq(prec, A, b, nthreads=cores)
+    dt = (time.perf_counter() - t0) / repeats
+    flops = ledger_flops(prec, M, K, nb, form_q=False)["total_flops"]
+    return {"value": round(flops / dt / 1e9, 4), "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
+            "sample": f"{repeats} full {prec} {M}x{K} least-squares solve(s) (unblocked Householder QR, "
+                      f"Q^T b by reflectors, back substitution); flops = ledger count of the no-Q pipeline",
+            "seconds_per_solve": round(dt, 3)}
+
+
+def run_reference(args, ws, rank, local):
+    """--impl reference: the oracle as it stands, on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    import oracle
+
+    prec, M, K, nb = WORKLOADS[args.workload]
+    oracle.build()
+    cores = oracle.default_threads()
+    A, b = make_problem(prec, M, K, 0)
+    for _ in range(args.warmup):
+        oracle.lstsq(prec, A, b, nthreads=cores)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.lstsq(prec, A, b, nthreads=cores)
+    dt = (time.perf_counter() - t0) / args.steps
+    flops = ledger_flops(prec, M, K, nb, form_q=False)["total_flops"]
+    v = round(flops / dt / 1e9, 4)
+    res = {
+        "metric": METRIC, "value": v, "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{prec} least squares {M}x{K}, tile {nb} (oracle: unblocked QR + Q^T b + BS)",
+                   "precision": prec, "M": M, "K": K, "nb": nb},
+        "impl": "reference",
+        "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
+                         "sample": f"each step one full {prec} {M}x{K} solve"},
+        "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(res), flush=True)
+
+
+def main():
+    args = parse()
+    ws, rank, local = dist_env()
+    if args.gpus != ws and ws > 1:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {ws}", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args, ws, rank, local)
+    else:
+        run_ours(args, ws, rank, local)
+
+
+if __name__ == "__main__":
+    main()

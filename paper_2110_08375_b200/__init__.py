@@ -1,0 +1,236 @@
+"""Multiple-double least squares on B200 (arXiv 2110.08375), Python binding.
+
+Thin marshalling over the C-ABI of ``include/mdls.h`` (``libmdls.so``): every
+step of the path runs in the library's sm_100a kernels; torch only supplies
+device memory and the current CUDA stream.  There is no CPU fallback.
+
+Layout (the paper's staggered storage): an md matrix with ``ld``
+rows and ``cols`` columns is a CUDA float64 tensor of shape ``(m, cols, ld)``
+(limb planes, most significant first, each column-major); an md vector of
+length n is ``(m, n)``.  m = 2 (dd), 4 (qd), 8 (od).
+"""
+from __future__ import annotations
+
+import ctypes
+
+from . import _lib
+
+PRECISIONS = {"dd": 2, "qd": 4, "od": 8}
+OPS = {"add": 0, "sub": 1, "mul": 2, "div": 3, "sqrt": 4}
+T1_SUMS = {"dd": (20, 23, 70), "qd": (89, 336, 893), "od": (269, 1742, 5126)}  # P:102-136 (add, mul, div)
+
+__all__ = ["md_op", "qr", "apply_qt", "qt_b", "invert_tiles", "backsub", "lstsq", "counts", "workspace_bytes",
+           "PRECISIONS"]
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _stream():
+    torch = _torch()
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _check_md(t, prec, ndim, name):
+    torch = _torch()
+    m = PRECISIONS[prec]
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name}: expected a CUDA tensor")
+    if t.dtype != torch.float64 or t.dim() != ndim or t.shape[0] != m or not t.is_contiguous():
+        raise ValueError(f"{name}: expected contiguous float64 of {ndim} dims with {m} limb planes, got "
+                         f"{tuple(t.shape)} {t.dtype}")
+
+
+def _mat(t):
+    """(ptr, ld, ps) of an (m, cols, ld) tensor"""
+    return ctypes.c_void_p(t.data_ptr()), t.shape[2], t.shape[1] * t.shape[2]
+
+
+def _vec(t):
+    return ctypes.c_void_p(t.data_ptr()), t.shape[1]
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr() if t is not None else 0)
+
+
+def workspace_bytes(prec: str, op: int, M: int, K: int, nb: int) -> int:
+    return int(_lib.fn("mdls_workspace_", prec)(op, M, K, nb))
+
+
+def _work(prec, op, M, K, nb, device):
+    torch = _torch()
+    n = workspace_bytes(prec, op, M, K, nb)
+    if n == 0:
+        raise ValueError(f"invalid sizes M={M} K={K} nb={nb}")
+    return torch.empty(n, dtype=torch.uint8, device=device), n
+
+
+def _info(device):
+    torch = _torch()
+    return torch.zeros(1, dtype=torch.int32, device=device)
+
+
+def md_op(op: str, prec: str, a, b=None):
+    """Elementwise md arithmetic on (m, n) CUDA vectors (A0)."""
+    torch = _torch()
+    _check_md(a, prec, 2, "a")
+    if op != "sqrt":
+        _check_md(b, prec, 2, "b")
+    c = torch.empty_like(a)
+    n = a.shape[1]
+    rc = _lib.fn("mdls_md_op_", prec)(OPS[op], n, _ptr(a), _ptr(b if op != "sqrt" else None), _ptr(c), n, _stream())
+    _lib.check(rc, "md_op")
+    return c
+
+
+def qr(prec: str, A, nb: int, form_q: bool = True, want_w: bool = False):
+    """Blocked Householder QR (Algorithm 2).  Returns (F, Q, W, info): F = factored
+    copy of A (R upper, v below), Q (m, M, M) or None, W (m, K, M) or None,
+    info a device int32 tensor (0 ok, k>0 first zero/non-finite R_kk)."""
+    torch = _torch()
+    _check_md(A, prec, 3, "A")
+    m, K, M = A.shape
+    F = A.clone()
+    Q = torch.empty((m, M, M), dtype=torch.float64, device=A.device) if form_q else None
+    W = torch.empty((m, K, M), dtype=torch.float64, device=A.device) if want_w else None
+    work, nbytes = _work(prec, _lib.OP_QR, M, K, nb, A.device)
+    info = _info(A.device)
+    qp, qld, qps = _mat(Q) if Q is not None else (ctypes.c_void_p(0), 0, 0)
+    wp, wld, wps = _mat(W) if W is not None else (ctypes.c_void_p(0), 0, 0)
+    rc = _lib.fn("mdls_qr_", prec)(M, K, nb, *_mat(F), qp, qld, qps, wp, wld, wps, _ptr(work), nbytes,
+                                   _ptr(info), _stream())
+    _lib.check(rc, "qr")
+    return F, Q, W, info
+
+
+def apply_qt(prec: str, F, W, b, nb: int):
+    """y = Q^T b from a factored F and its W (panels applied)."""
+    torch = _torch()
+    _check_md(F, prec, 3, "F")
+    _check_md(b, prec, 2, "b")
+    m, K, M = F.shape
+    y = torch.empty_like(b)
+    work, nbytes = _work(prec, _lib.OP_APPLY_QT, M, K, nb, F.device)
+    rc = _lib.fn("mdls_apply_qt_", prec)(M, K, nb, *_mat(F), *_mat(W), *_vec(b), *_vec(y), _ptr(work), nbytes,
+                                         _stream())
+    _lib.check(rc, "apply_qt")
+    return y
+
+
+def qt_b(prec: str, Q, b):
+    """y = Q^T b with an explicit Q."""
+    torch = _torch()
+    _check_md(Q, prec, 3, "Q")
+    _check_md(b, prec, 2, "b")
+    M = Q.shape[1]
+    y = torch.empty_like(b)
+    work = torch.empty(8 * PRECISIONS[prec] * 8 * M, dtype=torch.uint8, device=Q.device)
+    rc = _lib.fn("mdls_qt_b_", prec)(M, *_mat(Q), *_vec(b), *_vec(y), _ptr(work), work.numel(), _stream())
+    _lib.check(rc, "qt_b")
+    return y
+
+
+def invert_tiles(prec: str, U, nb: int, n: int | None = None):
+    """Transposed inverses of the n/nb diagonal tiles of U (A7): Vt (m, n, nb)."""
+    torch = _torch()
+    _check_md(U, prec, 3, "U")
+    n = U.shape[1] if n is None else n
+    Vt = torch.empty((PRECISIONS[prec], n, nb), dtype=torch.float64, device=U.device)
+    info = _info(U.device)
+    rc = _lib.fn("mdls_invert_tiles_", prec)(n, nb, *_mat(U), *_mat(Vt), _ptr(info), _stream())
+    _lib.check(rc, "invert_tiles")
+    return Vt, info
+
+
+def backsub(prec: str, U, y, nb: int, n: int | None = None):
+    """Tiled back substitution (Algorithm 1) on the leading n x n of U.  Returns (x, info)."""
+    torch = _torch()
+    _check_md(U, prec, 3, "U")
+    _check_md(y, prec, 2, "y")
+    n = U.shape[1] if n is None else n
+    x = torch.empty((PRECISIONS[prec], n), dtype=torch.float64, device=U.device)
+    work, nbytes = _work(prec, _lib.OP_BACKSUB, n, n, nb, U.device)
+    info = _info(U.device)
+    rc = _lib.fn("mdls_backsub_", prec)(n, nb, *_mat(U), *_vec(y), *_vec(x), _ptr(work), nbytes, _ptr(info),
+                                        _stream())
+    _lib.check(rc, "backsub")
+    return x, info
+
+
+class LstsqResult:
+    __slots__ = ("x", "R", "Q", "y", "info")
+
+    def __init__(self, x, R, Q, y, info):
+        self.x, self.R, self.Q, self.y, self.info = x, R, Q, y, info
+
+
+def lstsq(prec: str, A, b, nb: int, form_q: bool = True, want_R: bool = False, want_Q: bool = False,
+          want_y: bool = False, work=None):
+    """Least squares x = argmin ||b - A x|| (QR, Q^T b, tiled back substitution)."""
+    torch = _torch()
+    _check_md(A, prec, 3, "A")
+    _check_md(b, prec, 2, "b")
+    m, K, M = A.shape
+    dev = A.device
+    x = torch.empty((m, K), dtype=torch.float64, device=dev)
+    R = torch.empty((m, K, M), dtype=torch.float64, device=dev) if want_R else None
+    Q = torch.empty((m, M, M), dtype=torch.float64, device=dev) if (want_Q and form_q) else None
+    y = torch.empty((m, M), dtype=torch.float64, device=dev) if want_y else None
+    op = _lib.OP_LSTSQ if form_q else _lib.OP_LSTSQ_NOQ
+    if work is None:
+        work, nbytes = _work(prec, op, M, K, nb, dev)
+    else:
+        nbytes = work.numel()
+    info = _info(dev)
+    rp = _mat(R) if R is not None else (ctypes.c_void_p(0), 0, 0)
+    qp = _mat(Q) if Q is not None else (ctypes.c_void_p(0), 0, 0)
+    yp = _vec(y) if y is not None else (ctypes.c_void_p(0), 0)
+    rc = _lib.fn("mdls_lstsq_", prec)(M, K, nb, *_mat(A), *_vec(b), *_vec(x), int(form_q), *rp, *qp, *yp,
+                                      _ptr(work), nbytes, _ptr(info), _stream())
+    _lib.check(rc, "lstsq")
+    return LstsqResult(x, R, Q, y, info)
+
+
+def launch_count() -> int:
+    """Kernels launched by libmdls since load (host counter)."""
+    return int(_lib.load().mdls_launch_count())
+
+
+def trace_enable(on: bool = True) -> None:
+    """Bracket every library launch with CUDA events (per-stage kernel times)."""
+    _lib.load().mdls_trace_enable(int(on))
+
+
+def trace_collect() -> dict:
+    """Per-stage and per-kernel-family event times (ms) of the traced launches."""
+    import numpy as np
+
+    st = np.zeros(_lib.NSTAGES + 1)
+    fm = np.zeros(len(_lib.FAMILIES))
+    fl = np.zeros(len(_lib.FAMILIES), dtype=np.int64)
+    rc = _lib.load().mdls_trace_collect(ctypes.c_void_p(st.ctypes.data), ctypes.c_void_p(fm.ctypes.data),
+                                        ctypes.c_void_p(fl.ctypes.data))
+    if rc < 0:
+        raise RuntimeError(f"trace_collect failed rc={rc}")
+    return {
+        "stages_ms": {s: float(v) for s, v in zip(_lib.STAGES + ("setup",), st)},
+        "family_ms": {f: float(v) for f, v in zip(_lib.FAMILIES, fm)},
+        "family_launches": {f: int(v) for f, v in zip(_lib.FAMILIES, fl)},
+        "launches": int(rc),
+    }
+
+
+def counts(prec: str, op: int, M: int, K: int, nb: int) -> dict:
+    """Canonical md-op counts and Table-1 flops per stage (host, A10 ledger)."""
+    c = _lib.Counts()
+    rc = _lib.fn("mdls_count_", prec)(op, M, K, nb, ctypes.byref(c))
+    _lib.check(rc, "count")
+    return {
+        "stages": {s: {"add": c.add[i], "mul": c.mul[i], "div": c.div[i], "sqrt": c.sqrt[i], "flops": c.flops[i]}
+                   for i, s in enumerate(_lib.STAGES)},
+        "total_flops": c.total_flops,
+    }

@@ -1,0 +1,252 @@
+// api.cuh -- the extern "C" entry points of include/mdls.h for one precision.
+// Included by api_dd.cu / api_qd.cu / api_od.cu with MDLS_P (dd|qd|od) and
+// MDLS_M (2|4|8) defined; argument checking, workspace carving, launches.
+#pragma once
+#include "solver.cuh"
+
+#define MDLS_CAT2(a, b) a##b
+#define MDLS_CAT(a, b) MDLS_CAT2(a, b)
+#define MDLS_FN(name) MDLS_CAT(name, MDLS_P)
+
+namespace mdls {
+namespace api_impl {
+
+constexpr int M = MDLS_M;
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+inline int launched() { return cudaGetLastError() == cudaSuccess ? 0 : MDLS_ERR_CUDA; }
+
+template <typename T>
+inline T* at(void* work, size_t off) {
+  return reinterpret_cast<T*>(static_cast<char*>(work) + off);
+}
+
+// plane strides must cover the operand
+inline bool mat_ok(const void* p, int64_t rows, int64_t cols, int64_t ld, int64_t ps) {
+  return p && ld >= std::max<int64_t>(1, rows) && ps >= ld * cols;
+}
+
+inline int tile_ok(int64_t Mr, int64_t K, int64_t nb) {
+  if (K < 1) return -2;
+  if (Mr < K) return -1;
+  if (nb < 1 || nb > 256 || K % nb != 0) return -3;
+  return 0;
+}
+
+}  // namespace api_impl
+}  // namespace mdls
+
+using namespace mdls;
+using namespace mdls::api_impl;
+
+extern "C" {
+
+size_t MDLS_FN(mdls_workspace_)(int op, int64_t Mr, int64_t K, int64_t nb) {
+  if (op == MDLS_OP_BACKSUB) {
+    if (K < 1 || nb < 1 || nb > 256 || K % nb) return 0;
+    return make_plan<M>(op, K, K, nb).total;
+  }
+  if (tile_ok(Mr, K, nb)) return 0;
+  return make_plan<M>(op, Mr, K, nb).total;
+}
+
+int MDLS_FN(mdls_md_op_)(int op, int64_t n, const double* a, const double* b, double* c, int64_t ps, void* stream) {
+  if (op < 0 || op > 4) return -1;
+  if (n < 0) return -2;
+  if (n == 0) return 0;
+  if (!a) return -3;
+  if (!b && op != 4) return -4;
+  if (!c) return -5;
+  if (ps < n) return -6;
+  MDLS_LAUNCH(F_MISC, S(stream), md_op_kernel<M><<<grid_for(n, 128), 128, 0, S(stream)>>>(op, n, a, b, c, ps));
+  return launched();
+}
+
+int MDLS_FN(mdls_invert_tiles_)(int64_t n, int64_t nb, const double* U, int64_t ldu, int64_t psu, double* Vt,
+                                int64_t ldv, int64_t psv, int* dev_info, void* stream) {
+  if (n < 1) return -1;
+  if (nb < 1 || nb > 256 || n % nb) return -2;
+  if (!mat_ok(U, n, n, ldu, psu)) return -3;
+  if (!mat_ok(Vt, nb, n, ldv, psv)) return -6;
+  cudaStream_t st = S(stream);
+  set_stage(MDLS_NSTAGES);
+  int* slot = nullptr;
+  if (dev_info) {
+    slot = dev_info;
+    MDLS_LAUNCH(F_MISC, st, info_init_kernel<<<1, 1, 0, st>>>(slot));
+  } else {
+    return -9;
+  }
+  launch_invert<M>(st, n / nb, nb, CMat{U, ldu, psu}, Mat{Vt, ldv, psv}, 1.0, nullptr, slot);
+  MDLS_LAUNCH(F_MISC, st, info_finish_kernel<<<1, 1, 0, st>>>(slot, nullptr, dev_info));
+  return launched();
+}
+
+int MDLS_FN(mdls_backsub_)(int64_t n, int64_t nb, const double* U, int64_t ldu, int64_t psu, const double* y,
+                           int64_t psy, double* x, int64_t psx, void* work, size_t work_bytes, int* dev_info,
+                           void* stream) {
+  if (n < 1) return -1;
+  if (nb < 1 || nb > 256 || n % nb) return -2;
+  if (!mat_ok(U, n, n, ldu, psu)) return -3;
+  if (!y || psy < n) return -6;
+  if (!x || psx < n) return -8;
+  const Plan p = make_plan<M>(MDLS_OP_BACKSUB, n, n, nb);
+  if (!work || work_bytes < p.total) return -10;
+  cudaStream_t st = S(stream);
+  set_stage(MDLS_NSTAGES);
+  int* slot = at<int>(work, p.info);
+  MDLS_LAUNCH(F_MISC, st, info_init_kernel<<<1, 1, 0, st>>>(slot));
+  backsub<M>(st, n, nb, CMat{U, ldu, psu}, y, psy, x, psx, Mat{at<double>(work, p.vt), nb, nb * n},
+             at<double>(work, p.v0), slot);
+  if (dev_info) MDLS_LAUNCH(F_MISC, st, info_finish_kernel<<<1, 1, 0, st>>>(slot, nullptr, dev_info));
+  return launched();
+}
+
+static QrBufs<M> qr_bufs(void* work, const Plan& p, int64_t Mr, int64_t K, int64_t nb, double* W, int64_t ldw,
+                         int64_t psw) {
+  QrBufs<M> b;
+  b.Y = Mat{at<double>(work, p.y), Mr, Mr * K};
+  b.W = W ? Mat{W, ldw, psw} : Mat{at<double>(work, p.w), Mr, Mr * K};
+  b.beta = at<double>(work, p.beta);
+  b.S = Mat{at<double>(work, p.s), nb, nb * nb};
+  b.T = Mat{at<double>(work, p.t), nb, nb * nb};
+  const int64_t mx = std::max(Mr, K);
+  b.X = Mat{at<double>(work, p.x), nb, nb * mx};
+  b.part = at<double>(work, p.part);
+  b.part_cap = kMaxSplit * nb * mx;
+  b.info_slot = at<int>(work, p.info);
+  return b;
+}
+
+int MDLS_FN(mdls_qr_)(int64_t Mr, int64_t K, int64_t nb, double* A, int64_t lda, int64_t psa, double* Q, int64_t ldq,
+                      int64_t psq, double* W, int64_t ldw, int64_t psw, void* work, size_t work_bytes, int* dev_info,
+                      void* stream) {
+  if (int e = tile_ok(Mr, K, nb)) return e;
+  if (!mat_ok(A, Mr, K, lda, psa)) return -4;
+  if (Q && !mat_ok(Q, Mr, Mr, ldq, psq)) return -7;
+  if (W && !mat_ok(W, Mr, K, ldw, psw)) return -10;
+  const Plan p = make_plan<M>(MDLS_OP_QR, Mr, K, nb);
+  if (!work || work_bytes < p.total) return -14;
+  cudaStream_t st = S(stream);
+  set_stage(MDLS_NSTAGES);
+  QrBufs<M> b = qr_bufs(work, p, Mr, K, nb, W, ldw, psw);
+  MDLS_LAUNCH(F_MISC, st, info_init_kernel<<<1, 1, 0, st>>>(b.info_slot));
+  MDLS_LAUNCH(F_MISC, st, info_init_kernel<<<1, 1, 0, st>>>(b.info_slot + 1));
+  cudaMemsetAsync(b.Y.p, 0, sizeof(double) * M * Mr * K, st);
+  if (W) {
+    for (int l = 0; l < M; ++l) cudaMemset2DAsync(W + l * psw, sizeof(double) * ldw, 0, sizeof(double) * Mr, K, st);
+  } else {
+    cudaMemsetAsync(b.W.p, 0, sizeof(double) * M * Mr * K, st);
+  }
+  Mat Am{A, lda, psa};
+  if (qr_factor<M>(st, Mr, K, nb, Am, b, 0, K / nb, true) != cudaSuccess) return MDLS_ERR_CUDA;
+  if (Q) form_q_backward<M>(st, Mr, K, nb, Mat{Q, ldq, psq}, b);
+  if (dev_info) MDLS_LAUNCH(F_MISC, st, info_finish_kernel<<<1, 1, 0, st>>>(b.info_slot, nullptr, dev_info));
+  return launched();
+}
+
+int MDLS_FN(mdls_apply_qt_)(int64_t Mr, int64_t K, int64_t nb, const double* A, int64_t lda, int64_t psa,
+                            const double* W, int64_t ldw, int64_t psw, const double* b, int64_t psb, double* y,
+                            int64_t psy, void* work, size_t work_bytes, void* stream) {
+  if (int e = tile_ok(Mr, K, nb)) return e;
+  if (!mat_ok(A, Mr, K, lda, psa)) return -4;
+  if (!mat_ok(W, Mr, K, ldw, psw)) return -7;
+  if (!b || psb < Mr) return -10;
+  if (!y || psy < Mr) return -12;
+  const Plan p = make_plan<M>(MDLS_OP_APPLY_QT, Mr, K, nb);
+  if (!work || work_bytes < p.total) return -15;
+  cudaStream_t st = S(stream);
+  set_stage(MDLS_NSTAGES);
+  Mat Y{at<double>(work, p.y), Mr, Mr * K};
+  MDLS_LAUNCH(F_MISC, st, extract_y_kernel<M><<<grid_for(Mr * K, 256), 256, 0, st>>>(Mr, K, CMat{A, lda, psa}, Y));
+  double* yv = y;
+  if (y != b) MDLS_LAUNCH(F_MISC, st, copy_kernel<M><<<grid_for(Mr, 256), 256, 0, st>>>(Mr, 1, CMat{b, Mr, psb}, Mat{y, Mr, psy}, 0));
+  const int64_t mx = std::max(Mr, K);
+  apply_qt_panels<M>(st, Mr, K, nb, cm(Y), CMat{W, ldw, psw}, Mat{yv, Mr, psy}, Mat{at<double>(work, p.x), nb, nb * mx},
+                     at<double>(work, p.part), kMaxSplit * nb * mx);
+  return launched();
+}
+
+int MDLS_FN(mdls_qt_b_)(int64_t Mr, const double* Q, int64_t ldq, int64_t psq, const double* b, int64_t psb, double* y,
+                        int64_t psy, void* work, size_t work_bytes, void* stream) {
+  if (Mr < 1) return -1;
+  if (!mat_ok(Q, Mr, Mr, ldq, psq)) return -2;
+  if (!b || psb < Mr) return -5;
+  if (!y || psy < Mr || y == b) return -7;
+  cudaStream_t st = S(stream);
+  set_stage(MDLS_NSTAGES);
+  set_stage(MDLS_ST_QTB);
+  // no split-K partial buffer needed for correctness: pass the workspace when large enough
+  const size_t need = sizeof(double) * M * kMaxSplit * Mr;
+  double* part = (work && work_bytes >= need) ? static_cast<double*>(work) : nullptr;
+  gemm<M, true, false>(st, Mr, 1, Mr, CMat{Q, ldq, psq}, CMat{b, Mr, psb}, Mat{y, Mr, psy}, 0, part,
+                       part ? kMaxSplit * Mr : 0);
+  return launched();
+}
+
+int MDLS_FN(mdls_lstsq_)(int64_t Mr, int64_t K, int64_t nb, const double* A, int64_t lda, int64_t psa,
+                         const double* b, int64_t psb, double* x, int64_t psx, int form_q, double* R_out, int64_t ldr,
+                         int64_t psr, double* Q_out, int64_t ldq, int64_t psq, double* y_out, int64_t psy, void* work,
+                         size_t work_bytes, int* dev_info, void* stream) {
+  if (int e = tile_ok(Mr, K, nb)) return e;
+  if (!mat_ok(A, Mr, K, lda, psa)) return -4;
+  if (!b || psb < Mr) return -7;
+  if (!x || psx < K) return -9;
+  if (R_out && !mat_ok(R_out, Mr, K, ldr, psr)) return -12;
+  if (Q_out && !form_q) return -11;
+  if (Q_out && !mat_ok(Q_out, Mr, Mr, ldq, psq)) return -15;
+  if (y_out && psy < Mr) return -19;
+  const int op = form_q ? MDLS_OP_LSTSQ : MDLS_OP_LSTSQ_NOQ;
+  const Plan p = make_plan<M>(op, Mr, K, nb);
+  if (!work || work_bytes < p.total) return -21;
+  cudaStream_t st = S(stream);
+  set_stage(MDLS_NSTAGES);
+  QrBufs<M> bb = qr_bufs(work, p, Mr, K, nb, nullptr, 0, 0);
+  int* pre = bb.info_slot + 2;
+  MDLS_LAUNCH(F_MISC, st, info_init_kernel<<<1, 1, 0, st>>>(bb.info_slot));
+  MDLS_LAUNCH(F_MISC, st, info_init_kernel<<<1, 1, 0, st>>>(bb.info_slot + 1));
+  MDLS_LAUNCH(F_MISC, st, int_set_kernel<<<1, 1, 0, st>>>(pre, 0));
+  MDLS_LAUNCH(F_MISC, st, finite_check_kernel<M><<<grid_for(Mr * K, 256), 256, 0, st>>>(Mr, K, CMat{A, lda, psa}, pre));
+  MDLS_LAUNCH(F_MISC, st, finite_check_kernel<M><<<grid_for(Mr, 256), 256, 0, st>>>(Mr, 1, CMat{b, Mr, psb}, pre));
+  // factor a copy of A
+  Mat Af{at<double>(work, p.af), Mr, Mr * K};
+  MDLS_LAUNCH(F_MISC, st, copy_kernel<M><<<grid_for(Mr * K, 256), 256, 0, st>>>(Mr, K, CMat{A, lda, psa}, Af, 0));
+  cudaMemsetAsync(bb.Y.p, 0, sizeof(double) * M * Mr * K, st);
+  cudaMemsetAsync(bb.W.p, 0, sizeof(double) * M * Mr * K, st);
+  if (qr_factor<M>(st, Mr, K, nb, Af, bb, 0, K / nb, true) != cudaSuccess) return MDLS_ERR_CUDA;
+  double* yv = at<double>(work, p.v1);
+  if (form_q) {
+    Mat Q = Q_out ? Mat{Q_out, ldq, psq} : Mat{at<double>(work, p.q), Mr, Mr * Mr};
+    form_q_backward<M>(st, Mr, K, nb, Q, bb);
+    set_stage(MDLS_ST_QTB);
+    gemm<M, true, false>(st, Mr, 1, Mr, cm(Q), CMat{b, Mr, psb}, Mat{yv, Mr, Mr}, 0, bb.part, bb.part_cap);
+  } else {
+    MDLS_LAUNCH(F_MISC, st, copy_kernel<M><<<grid_for(Mr, 256), 256, 0, st>>>(Mr, 1, CMat{b, Mr, psb}, Mat{yv, Mr, Mr}, 0));
+    apply_qt_panels<M>(st, Mr, K, nb, cm(bb.Y), cm(bb.W), Mat{yv, Mr, Mr}, bb.X, bb.part, bb.part_cap);
+  }
+  backsub<M>(st, K, nb, cm(Af), yv, Mr, x, psx, Mat{at<double>(work, p.vt), nb, nb * K}, at<double>(work, p.v0),
+             bb.info_slot);
+  set_stage(MDLS_NSTAGES);
+  if (R_out) MDLS_LAUNCH(F_MISC, st, copy_kernel<M><<<grid_for(Mr * K, 256), 256, 0, st>>>(Mr, K, cm(Af), Mat{R_out, ldr, psr}, 1));
+  if (y_out) MDLS_LAUNCH(F_MISC, st, copy_kernel<M><<<grid_for(Mr, 256), 256, 0, st>>>(Mr, 1, CMat{yv, Mr, Mr}, Mat{y_out, Mr, psy}, 0));
+  if (dev_info) MDLS_LAUNCH(F_MISC, st, info_finish_kernel<<<1, 1, 0, st>>>(bb.info_slot, pre, dev_info));
+  return launched();
+}
+
+int MDLS_FN(mdls_qr_panel_)(int64_t Mr, int64_t K, int64_t nb, int64_t k, double* A, int64_t lda, int64_t psa,
+                            double* Wk, int64_t ldw, int64_t psw, double* Yk, int64_t ldy, int64_t psy, void* work,
+                            size_t work_bytes, int* dev_info, void* stream) {
+  (void)Mr; (void)K; (void)nb; (void)k; (void)A; (void)lda; (void)psa; (void)Wk; (void)ldw; (void)psw; (void)Yk;
+  (void)ldy; (void)psy; (void)work; (void)work_bytes; (void)dev_info; (void)stream;
+  return MDLS_ERR_UNSUPPORTED;
+}
+
+int MDLS_FN(mdls_qr_update_)(int64_t Mr, int64_t nb, int64_t k, const double* Wk, int64_t ldw, int64_t psw,
+                             const double* Yk, int64_t ldy, int64_t psy, double* A, int64_t lda, int64_t psa,
+                             int64_t c0, int64_t c1, void* work, size_t work_bytes, void* stream) {
+  (void)Mr; (void)nb; (void)k; (void)Wk; (void)ldw; (void)psw; (void)Yk; (void)ldy; (void)psy; (void)A; (void)lda;
+  (void)psa; (void)c0; (void)c1; (void)work; (void)work_bytes; (void)stream;
+  return MDLS_ERR_UNSUPPORTED;
+}
+
+}  // extern "C"

@@ -1,0 +1,7 @@
+// md GEMM instantiations for od (8 limbs).
+#include "kern_gemm.cuh"
+namespace mdls {
+MDLS_INSTANTIATE_GEMM(8, true, false)
+MDLS_INSTANTIATE_GEMM(8, false, true)
+MDLS_INSTANTIATE_GEMM(8, false, false)
+}  // namespace mdls

@@ -1,0 +1,156 @@
+// kern_bs.cuh -- tile inversion and tiled back substitution kernels (A7-A9).
+#pragma once
+#include "types.cuh"
+
+namespace mdls {
+
+// ============================================================================
+// A7: inverse of upper-triangular nb x nb tiles, one warp per inverse column
+// ("the k-th thread solves U v = e_k"; here the k-th WARP, its lanes
+// sharing the rows of the column-oriented back substitution).  Output is the
+// transposed inverse: Vt(c, tile*nb + r) = (U_tile^-1)(r, c).  diag_scale scales
+// the diagonal on read (0.5 builds the WY factor T from S = Y^T Y).  With
+// `dbeta` (leading limbs of the panel's beta), reflectors with beta = 0 (P = I,
+// GVL's sigma = 0 case) are decoupled: their row and column of U are treated as
+// zero off the diagonal and their column of the result is zero, which gives the
+// compact-WY factor of the remaining reflectors.
+// ============================================================================
+template <int M, int NPL>
+__global__ void __launch_bounds__(256) invert_tiles_kernel(int64_t nb, CMat U, Mat Vt, double diag_scale,
+                                                           const double* dbeta, int* info) {
+  extern __shared__ double smem_inv[];  // rinv: M planes of nb
+  const int tile = blockIdx.x;
+  const int64_t base = (int64_t)tile * nb;  // tile rows/cols offset
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
+
+  for (int64_t r = tid; r < nb; r += blockDim.x) {
+    md<M> d = ld<M>(U.p, U.ps, (base + r) + (base + r) * U.ld);
+    if (diag_scale != 1.0) d = scale_pow2<M>(d, diag_scale);
+    if (dbeta && dbeta[r] == 0.0) d = md_from<M>(1.0);
+    if (!(d.v[0] != 0.0) || !isfinite(d.v[0])) atomicMin(info, (int)(base + r + 1));
+    md<M> q = div<M>(md_from<M>(1.0), d);
+#pragma unroll
+    for (int l = 0; l < M; ++l) smem_inv[l * nb + r] = q.v[l];
+  }
+  __syncthreads();
+
+  for (int64_t k = (int64_t)blockIdx.y * nwarp + warp; k < nb; k += (int64_t)gridDim.y * nwarp) {
+    const bool degk = dbeta && dbeta[k] == 0.0;
+    md<M> s[NPL];
+#pragma unroll
+    for (int t = 0; t < NPL; ++t) s[t] = md_from<M>((lane + 32 * t == k) ? 1.0 : 0.0);
+    for (int64_t l = k; l >= 0; --l) {
+      const int ol = (int)(l & 31), tl = (int)(l >> 5);
+      md<M> sl = s[0];
+#pragma unroll
+      for (int t = 1; t < NPL; ++t)
+        if (t == tl) sl = s[t];
+      md<M> rinv;
+#pragma unroll
+      for (int q = 0; q < M; ++q) rinv.v[q] = smem_inv[q * nb + l];
+      md<M> x = mul<M>(sl, rinv);
+      x = shfl<M>(x, ol);
+      if (lane == 0) st<M>(Vt.p, Vt.ps, k + (base + l) * Vt.ld, degk ? md_zero<M>() : x);
+      const md<M> nx = neg(x);
+      const bool degl = dbeta && dbeta[l] == 0.0;
+#pragma unroll
+      for (int t = 0; t < NPL; ++t) {
+        const int64_t i = lane + 32 * t;
+        if (i < l) {
+          md<M> u = (degl || (dbeta && dbeta[i] == 0.0)) ? md_zero<M>()
+                                                           : ld<M>(U.p, U.ps, (base + i) + (base + l) * U.ld);
+          s[t] = fma<M>(s[t], u, nx);
+        }
+      }
+    }
+    // zeros below the diagonal of the inverse: Vt(k, base + r) for r > k
+    for (int64_t r = k + 1 + lane; r < nb; r += 32) st<M>(Vt.p, Vt.ps, k + (base + r) * Vt.ld, md_zero<M>());
+  }
+}
+
+// ============================================================================
+// A8: x_i = U_i^-1 b_i, one warp per output row (lanes over the columns)
+// ============================================================================
+template <int M>
+__global__ void __launch_bounds__(256) bs_mulinv_kernel(int64_t nb, int64_t tile, CMat Vt, const double* b,
+                                                        int64_t psb, double* x, int64_t psx) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= nb) return;
+  const int64_t base = tile * nb;
+  md<M> s = md_zero<M>();
+  for (int64_t c = r + lane; c < nb; c += 32) {  // upper triangular: c >= r
+    md<M> t = ld<M>(Vt.p, Vt.ps, c + (base + r) * Vt.ld);
+    md<M> bb = ld<M>(b, psb, base + c);
+    s = fma<M>(s, t, bb);
+  }
+  s = warp_sum<M>(s);
+  if (lane == 0) st<M>(x, psx, base + r, s);
+}
+
+// ============================================================================
+// A9: b(rho) -= sum_c U(rho, tile*nb + c) x_tile(c) for rho < tile*nb.
+// CTA = 32 rows x G column groups; fixed-order smem reduction over groups.
+// ============================================================================
+template <int M, int G>
+__global__ void __launch_bounds__(32 * G) bs_update_kernel(int64_t nb, int64_t tile, CMat U, const double* x,
+                                                           int64_t psx, double* b, int64_t psb) {
+  __shared__ md<M> part[G][32];
+  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int64_t rho = (int64_t)blockIdx.x * 32 + lane;
+  const int64_t nrows = tile * nb;
+  const int64_t base = tile * nb;
+  md<M> s = md_zero<M>();
+  if (rho < nrows) {
+    for (int64_t c = g; c < nb; c += G) {
+      md<M> u = ld<M>(U.p, U.ps, rho + (base + c) * U.ld);
+      md<M> xx = ld<M>(x, psx, base + c);
+      s = fma<M>(s, u, xx);
+    }
+  }
+  part[g][lane] = s;
+  __syncthreads();
+  if (g == 0 && rho < nrows) {
+    md<M> t = part[0][lane];
+#pragma unroll
+    for (int q = 1; q < G; ++q) t = add<M>(t, part[q][lane]);
+    md<M> bb = ld<M>(b, psb, rho);
+    st<M>(b, psb, rho, add<M>(bb, neg(t)));
+  }
+}
+
+
+template <int M>
+void launch_invert(cudaStream_t st, int64_t ntiles, int64_t nb, CMat U, Mat Vt, double diag_scale, const double* dbeta,
+                   int* info) {
+  const int threads = 256, nwarp = threads / 32;
+  const int64_t ny = cdiv(nb, nwarp);
+  dim3 grid((unsigned)ntiles, (unsigned)ny);
+  const size_t smem = sizeof(double) * M * nb;
+  if (nb <= 32) MDLS_LAUNCH(F_INVERT, st, invert_tiles_kernel<M, 1><<<grid, threads, smem, st>>>(nb, U, Vt, diag_scale, dbeta, info));
+  else if (nb <= 64) MDLS_LAUNCH(F_INVERT, st, invert_tiles_kernel<M, 2><<<grid, threads, smem, st>>>(nb, U, Vt, diag_scale, dbeta, info));
+  else if (nb <= 128) MDLS_LAUNCH(F_INVERT, st, invert_tiles_kernel<M, 4><<<grid, threads, smem, st>>>(nb, U, Vt, diag_scale, dbeta, info));
+  else MDLS_LAUNCH(F_INVERT, st, invert_tiles_kernel<M, 8><<<grid, threads, smem, st>>>(nb, U, Vt, diag_scale, dbeta, info));
+}
+
+template <int M>
+void launch_bs_mulinv(cudaStream_t st, int64_t nb, int64_t tile, CMat Vt, const double* b, int64_t psb, double* x,
+                      int64_t psx) {
+  MDLS_LAUNCH(F_BS, st, bs_mulinv_kernel<M><<<(unsigned)cdiv(nb, 8), 256, 0, st>>>(nb, tile, Vt, b, psb, x, psx));
+}
+
+template <int M>
+void launch_bs_update(cudaStream_t st, int64_t nb, int64_t tile, CMat U, const double* x, int64_t psx, double* b,
+                      int64_t psb) {
+  constexpr int G = 8;
+  MDLS_LAUNCH(F_BS, st, bs_update_kernel<M, G><<<(unsigned)cdiv(tile * nb, 32), 32 * G, 0, st>>>(nb, tile, U, x, psx, b, psb));
+}
+
+#define MDLS_INSTANTIATE_BS(MM)                                                                                \
+  template void launch_invert<MM>(cudaStream_t, int64_t, int64_t, CMat, Mat, double, const double*, int*);                    \
+  template void launch_bs_mulinv<MM>(cudaStream_t, int64_t, int64_t, CMat, const double*, int64_t, double*,    \
+                                     int64_t);                                                                 \
+  template void launch_bs_update<MM>(cudaStream_t, int64_t, int64_t, CMat, const double*, int64_t, double*,    \
+                                     int64_t);
+
+}  // namespace mdls

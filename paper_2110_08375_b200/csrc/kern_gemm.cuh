@@ -1,0 +1,153 @@
+// kern_gemm.cuh -- md GEMM on the FP64 pipe (trailing update, WY build, Q formation, Q^T b).
+#pragma once
+#include "types.cuh"
+
+namespace mdls {
+
+// ============================================================================
+// md GEMM on the FP64 pipe: C (mode)= op(A) op(B)
+//   op(A)(i, k) = TA ? A[k + i*lda] : A[i + k*lda]   (m x k)
+//   op(B)(k, j) = TB ? B[j + k*ldb] : B[k + j*ldb]   (k x n)
+// Shared-memory staged (limb-planar smem tiles), TM x TN register tile per
+// thread, one md mul + one md add per output and k.  Split-K: blockIdx.z takes
+// k range [z*kc, (z+1)*kc) and writes its partial tile to `part` (m x n per
+// split, ld m, split z at column offset z*n, plane stride m*n*S); a fixed-order
+// reduction kernel finishes.  mode: 0 C = P, 1 C += P, 2 C -= P, 3 C = -P.
+// ============================================================================
+template <int M>
+__device__ __forceinline__ md<M> apply_mode(int mode, const md<M>& c, const md<M>& p) {
+  switch (mode) {
+    case 0: return p;
+    case 1: return add<M>(c, p);
+    case 2: return add<M>(c, neg(p));
+    default: return neg(p);
+  }
+}
+
+template <int M, bool TA, bool TB>
+__global__ void __launch_bounds__((GemmCfg<M>::BM / GemmCfg<M>::TM) * (GemmCfg<M>::BN / GemmCfg<M>::TN))
+    gemm_kernel(GemmArgs g) {
+  constexpr int BM = GemmCfg<M>::BM, BN = GemmCfg<M>::BN, BK = GemmCfg<M>::BK;
+  constexpr int TM = GemmCfg<M>::TM, TN = GemmCfg<M>::TN;
+  constexpr int NX = BN / TN, NY = BM / TM, NT = NX * NY;
+  __shared__ double As[M][BK][BM];
+  __shared__ double Bs[M][BK][BN];
+
+  const int tid = threadIdx.x;
+  const int tx = tid % NX, ty = tid / NX;
+  const int64_t i0 = (int64_t)blockIdx.y * BM, j0 = (int64_t)blockIdx.x * BN;
+  const int64_t kb = (int64_t)blockIdx.z * g.kc;
+  const int64_t ke = min(g.k, kb + g.kc);
+
+  md<M> acc[TM][TN];
+#pragma unroll
+  for (int t = 0; t < TM; ++t)
+#pragma unroll
+    for (int u = 0; u < TN; ++u) acc[t][u] = md_zero<M>();
+
+  for (int64_t k0 = kb; k0 < ke; k0 += BK) {
+    // ---- stage A tile (BM x BK) ----
+    for (int e = tid; e < BM * BK; e += NT) {
+      int ii, kk;
+      if (TA) { kk = e % BK; ii = e / BK; } else { ii = e % BM; kk = e / BM; }
+      const int64_t gi = i0 + ii, gk = k0 + kk;
+      const bool ok = gi < g.m && gk < ke;
+      const int64_t off = TA ? (gk + gi * g.lda) : (gi + gk * g.lda);
+#pragma unroll
+      for (int l = 0; l < M; ++l) As[l][kk][ii] = ok ? g.A[l * g.psa + off] : 0.0;
+    }
+    // ---- stage B tile (BK x BN) ----
+    for (int e = tid; e < BK * BN; e += NT) {
+      int kk, jj;
+      if (TB) { jj = e % BN; kk = e / BN; } else { kk = e % BK; jj = e / BK; }
+      const int64_t gj = j0 + jj, gk = k0 + kk;
+      const bool ok = gj < g.n && gk < ke;
+      const int64_t off = TB ? (gj + gk * g.ldb) : (gk + gj * g.ldb);
+#pragma unroll
+      for (int l = 0; l < M; ++l) Bs[l][kk][jj] = ok ? g.B[l * g.psb + off] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 2
+    for (int kk = 0; kk < BK; ++kk) {
+      md<M> a[TM], b[TN];
+#pragma unroll
+      for (int t = 0; t < TM; ++t)
+#pragma unroll
+        for (int l = 0; l < M; ++l) a[t].v[l] = As[l][kk][ty + t * NY];
+#pragma unroll
+      for (int u = 0; u < TN; ++u)
+#pragma unroll
+        for (int l = 0; l < M; ++l) b[u].v[l] = Bs[l][kk][tx + u * NX];
+#pragma unroll
+      for (int t = 0; t < TM; ++t)
+#pragma unroll
+        for (int u = 0; u < TN; ++u) acc[t][u] = fma<M>(acc[t][u], a[t], b[u]);
+    }
+    __syncthreads();
+  }
+
+  // ---- epilogue ----
+#pragma unroll
+  for (int t = 0; t < TM; ++t) {
+    const int64_t gi = i0 + ty + t * NY;
+    if (gi >= g.m) continue;
+#pragma unroll
+    for (int u = 0; u < TN; ++u) {
+      const int64_t gj = j0 + tx + u * NX;
+      if (gj >= g.n) continue;
+      if (g.part) {
+        const int64_t pps = g.m * g.n * g.S;
+        st<M>(g.part, pps, gi + (gj + blockIdx.z * g.n) * g.m, acc[t][u]);
+      } else {
+        const int64_t e = gi + gj * g.ldc;
+        md<M> c = (g.mode == 1 || g.mode == 2) ? ld<M>(g.C, g.psc, e) : md_zero<M>();
+        st<M>(g.C, g.psc, e, apply_mode<M>(g.mode, c, acc[t][u]));
+      }
+    }
+  }
+}
+
+// C (mode)= sum_{z=0..S-1} part_z, in split order
+template <int M>
+__global__ void splitk_reduce_kernel(int64_t m, int64_t n, int64_t S, const double* __restrict__ part, double* C,
+                                     int64_t ldc, int64_t psc, int mode) {
+  const int64_t total = m * n, pps = m * n * S;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % m, j = e / m;
+    md<M> s = ld<M>(part, pps, e);
+    for (int64_t z = 1; z < S; ++z) s = add<M>(s, ld<M>(part, pps, i + (j + z * n) * m));
+    const int64_t ce = i + j * ldc;
+    md<M> c = (mode == 1 || mode == 2) ? ld<M>(C, psc, ce) : md_zero<M>();
+    st<M>(C, psc, ce, apply_mode<M>(mode, c, s));
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// GEMM launcher with split-K for long reductions
+// ---------------------------------------------------------------------------
+template <int M, bool TA, bool TB>
+void gemm(cudaStream_t st, int64_t m, int64_t n, int64_t k, CMat A, CMat B, Mat C, int mode, double* part,
+          int64_t part_cap_elems) {
+  using Cfg = GemmCfg<M>;
+  constexpr int NT = (Cfg::BM / Cfg::TM) * (Cfg::BN / Cfg::TN);
+  if (m <= 0 || n <= 0) return;
+  const int64_t tiles = cdiv(m, Cfg::BM) * cdiv(n, Cfg::BN);
+  int64_t S = 1;
+  if (part && k > 4 * Cfg::BK) {
+    S = std::min<int64_t>(kMaxSplit, std::max<int64_t>(1, (2 * kNumSMs) / tiles));
+    S = std::min<int64_t>(S, cdiv(k, 4 * Cfg::BK));
+    while (S > 1 && m * n * S > part_cap_elems) --S;
+  }
+  int64_t kc = cdiv(cdiv(k, S), Cfg::BK) * Cfg::BK;
+  S = std::max<int64_t>(1, cdiv(k, kc));
+  GemmArgs g{m, n, k, A.p, A.ld, A.ps, B.p, B.ld, B.ps, C.p, C.ld, C.ps, mode, kc, S > 1 ? part : nullptr, S};
+  dim3 grid((unsigned)cdiv(n, Cfg::BN), (unsigned)cdiv(m, Cfg::BM), (unsigned)S);
+  MDLS_LAUNCH(F_GEMM, st, gemm_kernel<M, TA, TB><<<grid, NT, 0, st>>>(g));
+  if (S > 1) MDLS_LAUNCH(F_GEMM, st, splitk_reduce_kernel<M><<<grid_for(m * n, 256), 256, 0, st>>>(m, n, S, part, C.p, C.ld, C.ps, mode));
+}
+
+#define MDLS_INSTANTIATE_GEMM(MM, TA, TB)                                                                   \
+  template void gemm<MM, TA, TB>(cudaStream_t, int64_t, int64_t, int64_t, CMat, CMat, Mat, int, double*, int64_t);
+
+}  // namespace mdls

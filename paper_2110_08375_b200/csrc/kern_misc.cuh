@@ -1,0 +1,94 @@
+// kern_misc.cuh -- elementwise md arithmetic and utility kernels.
+#pragma once
+#include "types.cuh"
+
+namespace mdls {
+
+// ============================================================================
+// A0: elementwise md arithmetic
+// ============================================================================
+template <int M>
+__global__ void md_op_kernel(int op, int64_t n, const double* __restrict__ a, const double* __restrict__ b,
+                             double* __restrict__ c, int64_t ps) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    md<M> x = ld<M>(a, ps, e), r;
+    md<M> y = (op == 4) ? md_zero<M>() : ld<M>(b, ps, e);
+    switch (op) {
+      case 0: r = add<M>(x, y); break;
+      case 1: r = sub<M>(x, y); break;
+      case 2: r = mul<M>(x, y); break;
+      case 3: r = div<M>(x, y); break;
+      default: r = sqrt<M>(x); break;
+    }
+    st<M>(c, ps, e, r);
+  }
+}
+
+// ============================================================================
+// utility kernels
+// ============================================================================
+// dst(i, j) = src(i, j) for i < rows, j < cols (all limbs); optional zero of the
+// strictly-lower part (i > j) -- used for R_out.
+template <int M>
+__global__ void copy_kernel(int64_t rows, int64_t cols, CMat src, Mat dst, int zero_lower) {
+  const int64_t total = rows * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % rows, j = e / rows;
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+      double v = src.p[k * src.ps + j * src.ld + i];
+      dst.p[k * dst.ps + j * dst.ld + i] = (zero_lower && i > j) ? 0.0 : v;
+    }
+  }
+}
+
+// explicit Y (unit lower trapezoidal) from a factored A: 0 above, 1 on, v below the diagonal
+template <int M>
+__global__ void extract_y_kernel(int64_t rows, int64_t cols, CMat a, Mat y) {
+  const int64_t total = rows * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % rows, j = e / rows;
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+      double v = (i > j) ? a.p[k * a.ps + j * a.ld + i] : ((i == j && k == 0) ? 1.0 : 0.0);
+      y.p[k * y.ps + j * y.ld + i] = v;
+    }
+  }
+}
+
+// Q = I on rows x cols
+template <int M>
+__global__ void set_identity_kernel(int64_t rows, int64_t cols, Mat q) {
+  const int64_t total = rows * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % rows, j = e / rows;
+#pragma unroll
+    for (int k = 0; k < M; ++k) q.p[k * q.ps + j * q.ld + i] = (k == 0 && i == j) ? 1.0 : 0.0;
+  }
+}
+
+// info <- -1 if any limb of the rows x cols operand is not finite
+template <int M>
+__global__ void finite_check_kernel(int64_t rows, int64_t cols, CMat a, int* info) {
+  const int64_t total = rows * cols;
+  bool bad = false;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % rows, j = e / rows;
+#pragma unroll
+    for (int k = 0; k < M; ++k) bad |= !isfinite(a.p[k * a.ps + j * a.ld + i]);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicExch(info, -1);
+}
+
+static __global__ void info_init_kernel(int* slot) { *slot = INT_MAX; }
+// dev_info = min-slot (1-based first failure) or 0; a -1 (non-finite input) wins
+static __global__ void info_finish_kernel(const int* slot, const int* pre, int* dev_info) {
+  int v = *slot;
+  int r = (v == INT_MAX) ? 0 : v;
+  if (pre && *pre == -1) r = -1;
+  *dev_info = r;
+}
+static __global__ void int_set_kernel(int* p, int v) { *p = v; }
+
+
+}  // namespace mdls

@@ -1,0 +1,404 @@
+// md.cuh -- device multiple-double arithmetic on the FP64 pipe (sm_100a).
+//
+// A multiple double is an unevaluated sum of M doubles, M = 2 (dd), 4 (qd),
+// 8 (od), most significant first.  The operation families
+// are the ones the paper names: QDlib for double double
+// and CAMPARY's generated quad/octo double code, held in M separate
+// scalar registers and force-inlined.  The exact
+// variants are the readings listed in DESIGN.md ("md arithmetic readings");
+// they are the variants whose base-operation tallies reproduce the paper's
+// Table 1, with one deliberate change: two_prod uses the FMA
+// (DMUL + DFMA) instead of Dekker's split, which returns the identical exact
+// pair (p, e) in 2 instead of 17 FP64 operations.
+//
+// Every operation is written with explicit __dadd_rn / __dsub_rn / __dmul_rn /
+// __fma_rn intrinsics so nvcc can never contract or reassociate an error-free
+// transformation.  Renormalisation is branch-free (selects, integer zero
+// tests) so warps never diverge inside the arithmetic.
+#pragma once
+#include <cstdint>
+
+namespace mdls {
+
+template <int M>
+struct md {
+  double v[M];
+};
+
+// ----------------------------------------------------------------------------
+// error-free transformations
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
+  double ss = __dadd_rn(a, b);
+  double bb = __dsub_rn(ss, a);
+  e = __dadd_rn(__dsub_rn(a, __dsub_rn(ss, bb)), __dsub_rn(b, bb));
+  s = ss;
+}
+
+// Fast2Sum, |a| >= |b| (or a == 0)
+__device__ __forceinline__ void quick_two_sum(double a, double b, double& s, double& e) {
+  double ss = __dadd_rn(a, b);
+  e = __dsub_rn(b, __dsub_rn(ss, a));
+  s = ss;
+}
+
+// exact product via the fused multiply-add: p + e == a*b
+__device__ __forceinline__ void two_prod(double a, double b, double& p, double& e) {
+  double pp = __dmul_rn(a, b);
+  e = __fma_rn(a, b, -pp);
+  p = pp;
+}
+
+__device__ __forceinline__ bool nonzero(double x) {
+  return (static_cast<unsigned long long>(__double_as_longlong(x)) << 1) != 0ull;
+}
+
+template <int M>
+__device__ __forceinline__ md<M> md_zero() {
+  md<M> r;
+#pragma unroll
+  for (int k = 0; k < M; ++k) r.v[k] = 0.0;
+  return r;
+}
+
+template <int M>
+__device__ __forceinline__ md<M> md_from(double d) {
+  md<M> r = md_zero<M>();
+  r.v[0] = d;
+  return r;
+}
+
+template <int M>
+__device__ __forceinline__ md<M> neg(const md<M>& a) {
+  md<M> r;
+#pragma unroll
+  for (int k = 0; k < M; ++k) r.v[k] = -a.v[k];
+  return r;
+}
+
+// exact scaling by a power of two
+template <int M>
+__device__ __forceinline__ md<M> scale_pow2(const md<M>& a, double p2) {
+  md<M> r;
+#pragma unroll
+  for (int k = 0; k < M; ++k) r.v[k] = __dmul_rn(a.v[k], p2);
+  return r;
+}
+
+// ----------------------------------------------------------------------------
+// double double (QDlib)
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ md<2> dd_add(const md<2>& a, const md<2>& b) {
+  double s1, s2, t1, t2;
+  two_sum(a.v[0], b.v[0], s1, s2);
+  two_sum(a.v[1], b.v[1], t1, t2);
+  s2 = __dadd_rn(s2, t1);
+  quick_two_sum(s1, s2, s1, s2);
+  s2 = __dadd_rn(s2, t2);
+  md<2> c;
+  quick_two_sum(s1, s2, c.v[0], c.v[1]);
+  return c;
+}
+
+__device__ __forceinline__ md<2> dd_mul(const md<2>& a, const md<2>& b) {
+  double p1, p2;
+  two_prod(a.v[0], b.v[0], p1, p2);
+  p2 = __dadd_rn(p2, __dadd_rn(__dmul_rn(a.v[0], b.v[1]), __dmul_rn(a.v[1], b.v[0])));
+  md<2> c;
+  quick_two_sum(p1, p2, c.v[0], c.v[1]);
+  return c;
+}
+
+__device__ __forceinline__ md<2> dd_mul_d(const md<2>& a, double b) {
+  double p1, p2;
+  two_prod(a.v[0], b, p1, p2);
+  p2 = __dadd_rn(p2, __dmul_rn(a.v[1], b));
+  md<2> c;
+  quick_two_sum(p1, p2, c.v[0], c.v[1]);
+  return c;
+}
+
+__device__ __forceinline__ md<2> dd_add_d(const md<2>& a, double b) {
+  double s1, s2;
+  two_sum(a.v[0], b, s1, s2);
+  s2 = __dadd_rn(s2, a.v[1]);
+  md<2> c;
+  quick_two_sum(s1, s2, c.v[0], c.v[1]);
+  return c;
+}
+
+// QDlib accurate division: three quotient digits
+static __device__ __noinline__ md<2> dd_div(const md<2>& a, const md<2>& b) {
+  double q1 = __ddiv_rn(a.v[0], b.v[0]);
+  md<2> r = dd_add(a, neg(dd_mul_d(b, q1)));
+  double q2 = __ddiv_rn(r.v[0], b.v[0]);
+  r = dd_add(r, neg(dd_mul_d(b, q2)));
+  double q3 = __ddiv_rn(r.v[0], b.v[0]);
+  md<2> q;
+  quick_two_sum(q1, q2, q.v[0], q.v[1]);
+  return dd_add_d(q, q3);
+}
+
+// QDlib sqrt: one Newton correction of the double reciprocal square root
+static __device__ __noinline__ md<2> dd_sqrt(const md<2>& a) {
+  if (a.v[0] == 0.0) return md_zero<2>();
+  double x = __ddiv_rn(1.0, __dsqrt_rn(a.v[0]));
+  double ax = __dmul_rn(a.v[0], x);
+  md<2> sq;
+  two_prod(ax, ax, sq.v[0], sq.v[1]);
+  md<2> d = dd_add(a, neg(sq));
+  md<2> c;
+  two_sum(ax, __dmul_rn(d.v[0], __dmul_rn(x, 0.5)), c.v[0], c.v[1]);
+  return c;
+}
+
+// ----------------------------------------------------------------------------
+// quad / octo double (CAMPARY fast family)
+// ----------------------------------------------------------------------------
+
+// fast_renorm2L<M+1, M>: bottom-up Fast2Sum sweep over f[0..M], then a
+// top-down sweep over its first M outputs that emits a limb whenever the
+// Fast2Sum error is nonzero; zero padded.  2M-1 Fast2Sums, branch-free.
+template <int M>
+__device__ __forceinline__ md<M> renorm(const double (&f)[M + 1]) {
+  double g[M + 1];
+  double s = f[M];
+#pragma unroll
+  for (int i = M - 1; i >= 0; --i) quick_two_sum(f[i], s, s, g[i + 1]);
+  g[0] = s;
+  md<M> r;
+#pragma unroll
+  for (int k = 0; k < M; ++k) r.v[k] = 0.0;
+  double eps = g[0];
+  int j = 0;
+#pragma unroll
+  for (int i = 1; i <= M - 1; ++i) {
+    double rr, e;
+    quick_two_sum(eps, g[i], rr, e);
+    const bool emit = nonzero(e);
+#pragma unroll
+    for (int k = 0; k < i; ++k) r.v[k] = (emit && j == k) ? rr : r.v[k];
+    j += emit ? 1 : 0;
+    eps = emit ? e : rr;
+  }
+#pragma unroll
+  for (int k = 0; k < M; ++k) r.v[k] = (j == k) ? eps : r.v[k];
+  return r;
+}
+
+// baileyAdd_fast<M,M,M>
+template <int M>
+__device__ __forceinline__ md<M> gen_add(const md<M>& a, const md<M>& b) {
+  double f[M + 1], e;
+  f[M] = 0.0;
+#pragma unroll
+  for (int i = M - 1; i >= 0; --i) {
+    two_sum(a.v[i], b.v[i], f[i], e);
+#pragma unroll
+    for (int j = i + 1; j < M; ++j) two_sum(f[j], e, f[j], e);
+    f[M] = __dadd_rn(f[M], e);
+  }
+  return renorm<M>(f);
+}
+
+template <int M>
+__device__ __forceinline__ void carry(double (&f)[M + 1], int n, double x) {
+#pragma unroll
+  for (int j = n + 1; j < M; ++j) two_sum(f[j], x, f[j], x);
+  f[M] = __dadd_rn(f[M], x);
+}
+
+// baileyMul_fast<M,LA,LB> with M output limbs (LA, LB in {1, M})
+template <int M, int LA, int LB>
+__device__ __forceinline__ md<M> gen_mul_gen(const double (&a)[LA], const double (&b)[LB]) {
+  double f[M + 1];
+  f[M] = 0.0;
+  {
+    bool first = true;
+#pragma unroll
+    for (int i = 0; i < LA; ++i) {
+      const int j = M - i;
+      if (j < 0 || j >= LB) continue;
+      double p = __dmul_rn(a[i], b[j]);
+      if (first) {
+        f[M] = p;
+        first = false;
+      } else {
+        f[M] = __dadd_rn(f[M], p);
+      }
+    }
+  }
+#pragma unroll
+  for (int n = M - 1; n >= 0; --n) {
+    bool have = false;
+#pragma unroll
+    for (int i = 0; i <= n; ++i) {
+      const int j = n - i;
+      if (i >= LA || j >= LB) continue;
+      double p, pe, e;
+      two_prod(a[i], b[j], p, pe);
+      if (!have) {
+        f[n] = p;
+        have = true;
+        carry<M>(f, n, pe);
+      } else {
+        two_sum(f[n], p, f[n], e);
+        carry<M>(f, n, pe);
+        carry<M>(f, n, e);
+      }
+    }
+    if (!have) f[n] = 0.0;
+  }
+  return renorm<M>(f);
+}
+
+template <int M>
+__device__ __forceinline__ md<M> gen_mul(const md<M>& a, const md<M>& b) {
+  return gen_mul_gen<M, M, M>(a.v, b.v);
+}
+
+template <int M>
+__device__ __forceinline__ md<M> gen_mul_d(const md<M>& a, double b) {
+  const double bb[1] = {b};
+  return gen_mul_gen<M, M, 1>(a.v, bb);
+}
+
+// long division: M+1 quotient digits (not inlined: off the hot loops, keeps code size down)
+template <int M>
+__device__ __noinline__ md<M> gen_div(const md<M>& a, const md<M>& b) {
+  double q[M + 1];
+  md<M> r = a;
+  q[0] = __ddiv_rn(a.v[0], b.v[0]);
+#pragma unroll
+  for (int i = 1; i <= M; ++i) {
+    md<M> t = gen_mul_d<M>(b, q[i - 1]);
+    r = gen_add<M>(r, neg(t));
+    q[i] = __ddiv_rn(r.v[0], b.v[0]);
+  }
+  return renorm<M>(q);
+}
+
+// QDlib-style Newton on 1/sqrt, ceil(log2 M)+1 iterations, result a*y
+template <int M>
+__device__ __noinline__ md<M> gen_sqrt(const md<M>& a) {
+  if (a.v[0] == 0.0) return md_zero<M>();
+  constexpr int iters = (M == 4) ? 3 : 4;
+  md<M> y = md_from<M>(__ddiv_rn(1.0, __dsqrt_rn(a.v[0])));
+  const md<M> h = scale_pow2(a, 0.5);
+  const md<M> half = md_from<M>(0.5);
+#pragma unroll
+  for (int it = 0; it < iters; ++it) {
+    md<M> t = gen_mul<M>(y, y);
+    t = gen_mul<M>(h, t);
+    t = gen_add<M>(half, neg(t));
+    t = gen_mul<M>(t, y);
+    y = gen_add<M>(y, t);
+  }
+  return gen_mul<M>(a, y);
+}
+
+// ----------------------------------------------------------------------------
+// precision dispatch
+// ----------------------------------------------------------------------------
+template <int M>
+__device__ __forceinline__ md<M> add(const md<M>& a, const md<M>& b) {
+  if constexpr (M == 2) return dd_add(a, b);
+  else return gen_add<M>(a, b);
+}
+template <int M>
+__device__ __forceinline__ md<M> sub(const md<M>& a, const md<M>& b) {
+  return add<M>(a, neg(b));
+}
+template <int M>
+__device__ __forceinline__ md<M> mul(const md<M>& a, const md<M>& b) {
+  if constexpr (M == 2) return dd_mul(a, b);
+  else return gen_mul<M>(a, b);
+}
+template <int M>
+__device__ __forceinline__ md<M> mul_d(const md<M>& a, double b) {
+  if constexpr (M == 2) return dd_mul_d(a, b);
+  else return gen_mul_d<M>(a, b);
+}
+template <int M>
+__device__ __forceinline__ md<M> div(const md<M>& a, const md<M>& b) {
+  if constexpr (M == 2) return dd_div(a, b);
+  else return gen_div<M>(a, b);
+}
+template <int M>
+__device__ __forceinline__ md<M> sqrt(const md<M>& a) {
+  if constexpr (M == 2) return dd_sqrt(a);
+  else return gen_sqrt<M>(a);
+}
+// acc + a*b  (md mul, then md add: one "pair")
+template <int M>
+__device__ __forceinline__ md<M> fma(const md<M>& acc, const md<M>& a, const md<M>& b) {
+  return add<M>(acc, mul<M>(a, b));
+}
+// acc - a*b
+template <int M>
+__device__ __forceinline__ md<M> fms(const md<M>& acc, const md<M>& a, const md<M>& b) {
+  return add<M>(acc, neg(mul<M>(a, b)));
+}
+
+// ----------------------------------------------------------------------------
+// limb-planar access: limb k of element e at p[k*ps + e]
+// ----------------------------------------------------------------------------
+template <int M>
+__device__ __forceinline__ md<M> ld(const double* __restrict__ p, int64_t ps, int64_t e) {
+  md<M> r;
+#pragma unroll
+  for (int k = 0; k < M; ++k) r.v[k] = p[k * ps + e];
+  return r;
+}
+template <int M>
+__device__ __forceinline__ md<M> ld_cg(const double* p, int64_t ps, int64_t e) {
+  md<M> r;
+#pragma unroll
+  for (int k = 0; k < M; ++k) r.v[k] = __ldcg(p + k * ps + e);
+  return r;
+}
+template <int M>
+__device__ __forceinline__ void st(double* __restrict__ p, int64_t ps, int64_t e, const md<M>& x) {
+#pragma unroll
+  for (int k = 0; k < M; ++k) p[k * ps + e] = x.v[k];
+}
+
+template <int M>
+__device__ __forceinline__ md<M> shfl(const md<M>& x, int src, unsigned mask = 0xffffffffu) {
+  md<M> r;
+#pragma unroll
+  for (int k = 0; k < M; ++k) r.v[k] = __shfl_sync(mask, x.v[k], src);
+  return r;
+}
+template <int M>
+__device__ __forceinline__ md<M> shfl_down(const md<M>& x, int d, unsigned mask = 0xffffffffu) {
+  md<M> r;
+#pragma unroll
+  for (int k = 0; k < M; ++k) r.v[k] = __shfl_down_sync(mask, x.v[k], d);
+  return r;
+}
+template <int M>
+__device__ __forceinline__ md<M> shfl_xor(const md<M>& x, int d, unsigned mask = 0xffffffffu) {
+  md<M> r;
+#pragma unroll
+  for (int k = 0; k < M; ++k) r.v[k] = __shfl_xor_sync(mask, x.v[k], d);
+  return r;
+}
+
+// warp sum in a fixed tree order (lane 0 holds the result; deterministic)
+template <int M>
+__device__ __forceinline__ md<M> warp_sum(md<M> x) {
+#pragma unroll 1
+  for (int d = 16; d >= 1; d >>= 1) x = add<M>(x, shfl_down<M>(x, d));
+  return x;
+}
+// warp sum broadcast to all lanes (butterfly; every lane gets the same bits only
+// if add is commutative bitwise -- it is not for CAMPARY add, so use warp_sum +
+// shfl when all lanes need the identical value)
+template <int M>
+__device__ __forceinline__ md<M> warp_sum_all(md<M> x) {
+  x = warp_sum<M>(x);
+  return shfl<M>(x, 0);
+}
+
+}  // namespace mdls

@@ -28,3 +28,22 @@ def cuda_available() -> bool:
         return torch.cuda.is_available()
     except Exception:  # pragma: no cover
         return False
+
+
+@pytest.fixture(scope="session")
+def dev():
+    import torch
+
+    assert torch.cuda.is_available(), "GPU test needs a CUDA device"
+    import paper_2110_08375_b200 as mdls  # noqa: F401  (fails loudly if libmdls.so is missing)
+    from paper_2110_08375_b200 import _lib
+
+    _lib.load()
+    return torch.device("cuda:0")
+
+
+@pytest.fixture(scope="session")
+def mdls():
+    import paper_2110_08375_b200 as m
+
+    return m

@@ -1,0 +1,76 @@
+"""A7-A9 parity: tile inversion and tiled back substitution (Algorithm 1,
+P:323-352) vs the oracle's plain back substitution on the same inputs."""
+import numpy as np
+import pytest
+import torch
+
+from paper_2110_08375_b200 import inputs
+
+from ._parity import U_OF, md_diff, vec_ok
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("prec", ["dd", "qd", "od"])
+@pytest.mark.parametrize("n,nb", [(32, 32), (96, 32), (256, 64), (384, 128)])
+def test_invert_tiles_vs_oracle(orc, mdls, dev, prec, n, nb):
+    U = inputs.lu_upper(n, prec, seed=n + nb)
+    Vt, info = mdls.invert_tiles(prec, torch.from_numpy(U).to(dev), nb)
+    torch.cuda.synchronize()
+    assert int(info.item()) == 0
+    Vt = Vt.cpu().numpy()  # (m, n, nb): Vt[:, t*nb + r, c] = (U_t^-1)(r, c)
+    m = U.shape[0]
+    for t in range(n // nb):
+        tile = np.ascontiguousarray(U[:, t * nb:(t + 1) * nb, t * nb:(t + 1) * nb])
+        for c in range(nb):
+            e = np.zeros((m, nb))
+            e[0, c] = 1.0
+            col, _ = orc.backsub(prec, tile, e)
+            got = np.ascontiguousarray(Vt[:, t * nb:(t + 1) * nb, c])
+            err, tol = vec_ok(orc, prec, got, col, nb)
+            assert err <= tol, (t, c, err, tol)
+
+
+@pytest.mark.parametrize("prec", ["dd", "qd", "od"])
+@pytest.mark.parametrize("n,nb", [(8, 8), (64, 8), (96, 32), (640, 128)])
+def test_backsub_vs_oracle(orc, mdls, dev, prec, n, nb):
+    U = inputs.lu_upper(n, prec, seed=7 * n + nb)
+    y = inputs.random_vector(n, prec, seed=n)
+    x, info = mdls.backsub(prec, torch.from_numpy(U).to(dev), torch.from_numpy(y).to(dev), nb)
+    torch.cuda.synchronize()
+    assert int(info.item()) == 0
+    xr, _ = orc.backsub(prec, U, y)
+    err, tol = vec_ok(orc, prec, x.cpu().numpy(), xr, n)
+    assert err <= tol, (err, tol)
+
+
+@pytest.mark.parametrize("prec", ["dd", "qd"])
+def test_backsub_identity_and_integer(orc, mdls, dev, prec):
+    m = inputs.limbs(prec)
+    n, nb = 64, 16
+    I = np.zeros((m, n, n))
+    I[0] = np.eye(n)
+    y = inputs.random_vector(n, prec, 3)
+    x, info = mdls.backsub(prec, torch.from_numpy(I).to(dev), torch.from_numpy(y).to(dev), nb)
+    assert np.array_equal(x.cpu().numpy(), y)
+    rng = np.random.default_rng(1)
+    Ui = np.triu(rng.integers(-2, 3, size=(n, n)).astype(float), 1) + np.eye(n)
+    xi = rng.integers(-3, 4, size=n).astype(float)
+    U = np.zeros((m, n, n))
+    U[0] = Ui.T
+    b = np.zeros((m, n))
+    b[0] = Ui @ xi
+    x, info = mdls.backsub(prec, torch.from_numpy(U).to(dev), torch.from_numpy(b).to(dev), nb)
+    got = x.cpu().numpy()
+    assert np.array_equal(got[0], xi) and np.all(got[1:] == 0)
+
+
+def test_backsub_singular_reports_row(mdls, dev):
+    m, n, nb = 2, 64, 16
+    U = np.zeros((m, n, n))
+    U[0] = np.eye(n)
+    U[0, 37, 37] = 0.0
+    y = np.ones((m, n))
+    x, info = mdls.backsub("dd", torch.from_numpy(U).to(dev), torch.from_numpy(y).to(dev), nb)
+    torch.cuda.synchronize()
+    assert int(info.item()) == 38
