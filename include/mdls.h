@@ -134,8 +134,9 @@ int mdls_trace_collect(double *stage_ms, double *family_ms, int64_t *family_laun
                         const double *W, int64_t ldw, int64_t psw, const double *b, int64_t psb, double *y,        \
                         int64_t psy, void *work, size_t work_bytes, void *stream);                                 \
                                                                                                                    \
-  /* y = Q^T b with an explicit M x M Q. b, y must not alias. */                                         \
-  int mdls_qt_b_##P(int64_t M, const double *Q, int64_t ldq, int64_t psq, const double *b, int64_t psb,            \
+  /* y = Q^T b with an explicit Q of M rows and N columns (N = M: the full Q; N < M: a column block,     \
+   * as in the column-sharded Q^T b).  b: length M, y: length N; b and y must not alias. */                        \
+  int mdls_qt_b_##P(int64_t M, int64_t N, const double *Q, int64_t ldq, int64_t psq, const double *b, int64_t psb,  \
                     double *y, int64_t psy, void *work, size_t work_bytes, void *stream);                          \
                                                                                                                    \
   /* A7: invert the N = n/nb diagonal nb x nb tiles of the upper-triangular U (leading n x n).          \
@@ -161,12 +162,16 @@ int mdls_trace_collect(double *stage_ms, double *family_ms, int64_t *family_laun
                      double *Q_out, int64_t ldq, int64_t psq, double *y_out, int64_t psy, void *work,              \
                      size_t work_bytes, int *dev_info, void *stream);                                              \
                                                                                                                    \
-  /* multi-GPU building blocks (block-column sharded QR): factor panel k (columns [k*nb, (k+1)*nb))       \
-   * of A and build its W and explicit Y (both M x nb operands, rows < k*nb zero). */                              \
-  int mdls_qr_panel_##P(int64_t M, int64_t K, int64_t nb, int64_t k, double *A, int64_t lda, int64_t psa,          \
-                        double *Wk, int64_t ldw, int64_t psw, double *Yk, int64_t ldy, int64_t psy, void *work,    \
+  /* multi-GPU building blocks (block-column sharded QR; host orchestration in sharded.py).           \
+   * qr_panel: factor panel k, i.e. the columns [k*nb, (k+1)*nb) of A passed as the M x nb operand Ak (rows        \
+   * 0..M-1, all earlier panels already applied), M >= (k+1)*nb; on return Ak holds R and v like mdls_qr, and     \
+   * Wk, Yk (M x nb, rows < k*nb zero) hold the panel's W and explicit Y (unit diagonal): P_WY = I + Wk Yk^T.      \
+   * dev_info as for mdls_qr (global 1-based row). */                                                              \
+  int mdls_qr_panel_##P(int64_t M, int64_t nb, int64_t k, double *Ak, int64_t lda, int64_t psa, double *Wk,        \
+                        int64_t ldw, int64_t psw, double *Yk, int64_t ldy, int64_t psy, void *work,                 \
                         size_t work_bytes, int *dev_info, void *stream);                                           \
-  /* apply panel k (Wk, Yk from mdls_qr_panel) to the column range [c0, c1) of A: C += Y (W^T C), rows >= k*nb. */  \
+  /* qr_update: C += Yk (Wk^T C) for the columns [c0, c1) of A, rows k*nb..M-1 ("YWT * C", "R + YWTC").            \
+   * With Wk and Yk exchanged it computes C += Wk (Yk^T C): the backward Q-formation step on a column block. */   \
   int mdls_qr_update_##P(int64_t M, int64_t nb, int64_t k, const double *Wk, int64_t ldw, int64_t psw,             \
                          const double *Yk, int64_t ldy, int64_t psy, double *A, int64_t lda, int64_t psa,          \
                          int64_t c0, int64_t c1, void *work, size_t work_bytes, void *stream);

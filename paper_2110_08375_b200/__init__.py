@@ -122,14 +122,14 @@ def apply_qt(prec: str, F, W, b, nb: int):
 
 
 def qt_b(prec: str, Q, b):
-    """y = Q^T b with an explicit Q."""
+    """y = Q^T b with an explicit Q of shape (m, N, M) (N columns of M rows); y has N entries."""
     torch = _torch()
     _check_md(Q, prec, 3, "Q")
     _check_md(b, prec, 2, "b")
-    M = Q.shape[1]
-    y = torch.empty_like(b)
-    work = torch.empty(8 * PRECISIONS[prec] * 8 * M, dtype=torch.uint8, device=Q.device)
-    rc = _lib.fn("mdls_qt_b_", prec)(M, *_mat(Q), *_vec(b), *_vec(y), _ptr(work), work.numel(), _stream())
+    m, N, M = Q.shape
+    y = torch.empty((m, N), dtype=torch.float64, device=Q.device)
+    work = torch.empty(8 * m * 8 * max(N, 1), dtype=torch.uint8, device=Q.device)
+    rc = _lib.fn("mdls_qt_b_", prec)(M, N, *_mat(Q), *_vec(b), *_vec(y), _ptr(work), work.numel(), _stream())
     _lib.check(rc, "qt_b")
     return y
 
@@ -234,3 +234,40 @@ def counts(prec: str, op: int, M: int, K: int, nb: int) -> dict:
                    for i, s in enumerate(_lib.STAGES)},
         "total_flops": c.total_flops,
     }
+
+
+# ---------------------------------------------------------------------------- multi-GPU building blocks
+def _view(t, col0: int, ncols: int):
+    """(ptr, ld, ps) of columns [col0, col0+ncols) of an (m, cols, ld) contiguous tensor."""
+    ld = t.shape[2]
+    return ctypes.c_void_p(t.data_ptr() + 8 * col0 * ld), ld, t.shape[1] * ld
+
+
+def qr_panel(prec: str, A, col0: int, k: int, nb: int, W, Y, work=None):
+    """Factor panel k stored in columns [col0, col0+nb) of A (rows global); W and Y
+    (m, nb, M) receive the panel's P_WY = I + W Y^T.  Returns the device info tensor."""
+    torch = _torch()
+    M = A.shape[2]
+    if work is None:
+        work, nbytes = _work(prec, _lib.OP_QR, M, nb, nb, A.device)
+    else:
+        nbytes = work.numel()
+    info = _info(A.device)
+    rc = _lib.fn("mdls_qr_panel_", prec)(M, nb, k, *_view(A, col0, nb), *_mat(W), *_mat(Y), _ptr(work), nbytes,
+                                         _ptr(info), _stream())
+    _lib.check(rc, "qr_panel")
+    return info
+
+
+def qr_update(prec: str, Wk, Yk, A, k: int, nb: int, c0: int, c1: int, work=None):
+    """C += Yk (Wk^T C) on columns [c0, c1) of A (rows k*nb..M-1)."""
+    M = A.shape[2]
+    if c1 <= c0:
+        return
+    if work is None:
+        work, nbytes = _work(prec, _lib.OP_QR, max(M, c1), max(c1, nb), nb, A.device)
+    else:
+        nbytes = work.numel()
+    rc = _lib.fn("mdls_qr_update_", prec)(M, nb, k, *_mat(Wk), *_mat(Yk), *_mat(A), c0, c1, _ptr(work), nbytes,
+                                          _stream())
+    _lib.check(rc, "qr_update")

@@ -42,12 +42,12 @@ _SIGS = {
     "mdls_md_op_": (_I, [_I, _L, _P, _P, _P, _L, _P]),
     "mdls_qr_": (_I, [_L, _L, _L, _P, _L, _L, _P, _L, _L, _P, _L, _L, _P, _Z, _P, _P]),
     "mdls_apply_qt_": (_I, [_L, _L, _L, _P, _L, _L, _P, _L, _L, _P, _L, _P, _L, _P, _Z, _P]),
-    "mdls_qt_b_": (_I, [_L, _P, _L, _L, _P, _L, _P, _L, _P, _Z, _P]),
+    "mdls_qt_b_": (_I, [_L, _L, _P, _L, _L, _P, _L, _P, _L, _P, _Z, _P]),
     "mdls_invert_tiles_": (_I, [_L, _L, _P, _L, _L, _P, _L, _L, _P, _P]),
     "mdls_backsub_": (_I, [_L, _L, _P, _L, _L, _P, _L, _P, _L, _P, _Z, _P, _P]),
     "mdls_lstsq_": (_I, [_L, _L, _L, _P, _L, _L, _P, _L, _P, _L, _I, _P, _L, _L, _P, _L, _L, _P, _L, _P, _Z, _P,
                          _P]),
-    "mdls_qr_panel_": (_I, [_L, _L, _L, _L, _P, _L, _L, _P, _L, _L, _P, _L, _L, _P, _Z, _P, _P]),
+    "mdls_qr_panel_": (_I, [_L, _L, _L, _P, _L, _L, _P, _L, _L, _P, _L, _L, _P, _Z, _P, _P]),
     "mdls_qr_update_": (_I, [_L, _L, _L, _P, _L, _L, _P, _L, _L, _P, _L, _L, _L, _L, _P, _Z, _P]),
 }
 

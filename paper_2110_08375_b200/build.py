@@ -16,7 +16,7 @@ CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libmdls.so")
 SOURCES = [f"{k}_{p}.cu" for p in ("od", "qd", "dd") for k in ("gemm", "panel", "bs", "api")] + ["ledger.cu"]
-HEADERS = ["md.cuh", "types.cuh", "launch.cuh", "kern_misc.cuh", "kern_gemm.cuh", "kern_panel.cuh", "kern_bs.cuh",
+HEADERS = ["md.cuh", "types.cuh", "launch.cuh", "kern_misc.cuh", "kern_gemm.cuh", "kern_leaf.cuh", "kern_bs.cuh",
            "solver.cuh", "api.cuh"]
 
 NVCC_FLAGS = [
@@ -55,7 +55,9 @@ def build(force: bool = False, verbose: bool = False, extra: list[str] | None = 
             if verbose:
                 cmd += ["-Xptxas", "-v"]
             jobs.append((s, cmd))
-    relink = bool(jobs) or not os.path.exists(LIB)
+    objs_all = [os.path.join(BUILD, s.replace(".cu", ".o")) for s in SOURCES]
+    relink = bool(jobs) or not os.path.exists(LIB) or any(
+        not os.path.exists(o) or os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs_all)
 
     def run(job):
         name, cmd = job

@@ -167,20 +167,21 @@ int MDLS_FN(mdls_apply_qt_)(int64_t Mr, int64_t K, int64_t nb, const double* A, 
   return launched();
 }
 
-int MDLS_FN(mdls_qt_b_)(int64_t Mr, const double* Q, int64_t ldq, int64_t psq, const double* b, int64_t psb, double* y,
-                        int64_t psy, void* work, size_t work_bytes, void* stream) {
+int MDLS_FN(mdls_qt_b_)(int64_t Mr, int64_t Nc, const double* Q, int64_t ldq, int64_t psq, const double* b,
+                        int64_t psb, double* y, int64_t psy, void* work, size_t work_bytes, void* stream) {
   if (Mr < 1) return -1;
-  if (!mat_ok(Q, Mr, Mr, ldq, psq)) return -2;
-  if (!b || psb < Mr) return -5;
-  if (!y || psy < Mr || y == b) return -7;
+  if (Nc < 0) return -2;
+  if (Nc == 0) return 0;
+  if (!mat_ok(Q, Mr, Nc, ldq, psq)) return -3;
+  if (!b || psb < Mr) return -6;
+  if (!y || psy < Nc || y == b) return -8;
   cudaStream_t st = S(stream);
-  set_stage(MDLS_NSTAGES);
   set_stage(MDLS_ST_QTB);
-  // no split-K partial buffer needed for correctness: pass the workspace when large enough
-  const size_t need = sizeof(double) * M * kMaxSplit * Mr;
+  // split-K partials go to the workspace when it is large enough
+  const size_t need = sizeof(double) * M * kMaxSplit * Nc;
   double* part = (work && work_bytes >= need) ? static_cast<double*>(work) : nullptr;
-  gemm<M, true, false>(st, Mr, 1, Mr, CMat{Q, ldq, psq}, CMat{b, Mr, psb}, Mat{y, Mr, psy}, 0, part,
-                       part ? kMaxSplit * Mr : 0);
+  gemm<M, true, false>(st, Nc, 1, Mr, CMat{Q, ldq, psq}, CMat{b, Mr, psb}, Mat{y, Nc, psy}, 0, part,
+                       part ? kMaxSplit * Nc : 0);
   return launched();
 }
 
@@ -233,20 +234,52 @@ int MDLS_FN(mdls_lstsq_)(int64_t Mr, int64_t K, int64_t nb, const double* A, int
   return launched();
 }
 
-int MDLS_FN(mdls_qr_panel_)(int64_t Mr, int64_t K, int64_t nb, int64_t k, double* A, int64_t lda, int64_t psa,
-                            double* Wk, int64_t ldw, int64_t psw, double* Yk, int64_t ldy, int64_t psy, void* work,
+int MDLS_FN(mdls_qr_panel_)(int64_t Mr, int64_t nb, int64_t k, double* Ak, int64_t lda, int64_t psa, double* Wk,
+                            int64_t ldw, int64_t psw, double* Yk, int64_t ldy, int64_t psy, void* work,
                             size_t work_bytes, int* dev_info, void* stream) {
-  (void)Mr; (void)K; (void)nb; (void)k; (void)A; (void)lda; (void)psa; (void)Wk; (void)ldw; (void)psw; (void)Yk;
-  (void)ldy; (void)psy; (void)work; (void)work_bytes; (void)dev_info; (void)stream;
-  return MDLS_ERR_UNSUPPORTED;
+  if (Mr < 1) return -1;
+  if (nb < 1 || nb > 256) return -2;
+  if (k < 0 || (k + 1) * nb > Mr) return -3;
+  if (!mat_ok(Ak, Mr, nb, lda, psa)) return -4;
+  if (!mat_ok(Wk, Mr, nb, ldw, psw)) return -7;
+  if (!mat_ok(Yk, Mr, nb, ldy, psy)) return -10;
+  const Plan p = make_plan<M>(MDLS_OP_QR, Mr, nb, nb);
+  if (!work || work_bytes < p.total) return -14;
+  cudaStream_t st = S(stream);
+  set_stage(MDLS_NSTAGES);
+  const int64_t j0 = k * nb;
+  // global-column views of the caller's M x nb panel buffers (column j -> j - j0)
+  Mat Ag{Ak - j0 * lda, lda, psa}, Wg{Wk - j0 * ldw, ldw, psw}, Yg{Yk - j0 * ldy, ldy, psy};
+  QrBufs<M> b = qr_bufs(work, p, Mr, nb, nb, nullptr, 0, 0);
+  MDLS_LAUNCH(F_MISC, st, info_init_kernel<<<1, 1, 0, st>>>(b.info_slot));
+  for (int l = 0; l < M; ++l) {
+    cudaMemset2DAsync(Wk + l * psw, sizeof(double) * ldw, 0, sizeof(double) * Mr, nb, st);
+    cudaMemset2DAsync(Yk + l * psy, sizeof(double) * ldy, 0, sizeof(double) * Mr, nb, st);
+  }
+  // beta: per panel, stored in the workspace (indexed by global column)
+  if (qr_panel<M>(st, Mr, nb, k, Ag, Yg, Wg, b.beta - j0, nb, b) != cudaSuccess) return MDLS_ERR_CUDA;
+  if (dev_info) MDLS_LAUNCH(F_MISC, st, info_finish_kernel<<<1, 1, 0, st>>>(b.info_slot, nullptr, dev_info));
+  return launched();
 }
 
 int MDLS_FN(mdls_qr_update_)(int64_t Mr, int64_t nb, int64_t k, const double* Wk, int64_t ldw, int64_t psw,
                              const double* Yk, int64_t ldy, int64_t psy, double* A, int64_t lda, int64_t psa,
                              int64_t c0, int64_t c1, void* work, size_t work_bytes, void* stream) {
-  (void)Mr; (void)nb; (void)k; (void)Wk; (void)ldw; (void)psw; (void)Yk; (void)ldy; (void)psy; (void)A; (void)lda;
-  (void)psa; (void)c0; (void)c1; (void)work; (void)work_bytes; (void)stream;
-  return MDLS_ERR_UNSUPPORTED;
+  if (Mr < 1) return -1;
+  if (nb < 1 || nb > 256) return -2;
+  if (k < 0 || (k + 1) * nb > Mr) return -3;
+  if (!mat_ok(Wk, Mr, nb, ldw, psw)) return -4;
+  if (!mat_ok(Yk, Mr, nb, ldy, psy)) return -7;
+  if (c0 < 0 || c1 < c0) return -13;
+  if (!mat_ok(A, Mr, c1, lda, psa)) return -10;
+  const Plan p = make_plan<M>(MDLS_OP_QR, std::max<int64_t>(Mr, c1), std::max<int64_t>(c1, nb), nb);
+  if (!work || work_bytes < p.total) return -16;
+  cudaStream_t st = S(stream);
+  set_stage(MDLS_NSTAGES);
+  QrBufs<M> b = qr_bufs(work, p, std::max<int64_t>(Mr, c1), std::max<int64_t>(c1, nb), nb, nullptr, 0, 0);
+  const int64_t j0 = k * nb;
+  qr_apply_panel<M>(st, Mr, nb, k, CMat{Yk + j0, ldy, psy}, CMat{Wk + j0, ldw, psw}, Mat{A, lda, psa}, c0, c1, b);
+  return launched();
 }
 
 }  // extern "C"

@@ -24,11 +24,11 @@ __device__ __forceinline__ md<M> apply_mode(int mode, const md<M>& c, const md<M
   }
 }
 
-template <int M, bool TA, bool TB>
-__global__ void __launch_bounds__((GemmCfg<M>::BM / GemmCfg<M>::TM) * (GemmCfg<M>::BN / GemmCfg<M>::TN))
-    gemm_kernel(GemmArgs g) {
-  constexpr int BM = GemmCfg<M>::BM, BN = GemmCfg<M>::BN, BK = GemmCfg<M>::BK;
-  constexpr int TM = GemmCfg<M>::TM, TN = GemmCfg<M>::TN;
+template <int M, int V, bool TA, bool TB>
+__global__ void __launch_bounds__(GemmTile<M, V>::NT) gemm_kernel(GemmArgs g) {
+  using Tl = GemmTile<M, V>;
+  constexpr int BM = Tl::BM, BN = Tl::BN, BK = Tl::BK;
+  constexpr int TM = Tl::TM, TN = Tl::TN;
   constexpr int NX = BN / TN, NY = BM / TM, NT = NX * NY;
   __shared__ double As[M][BK][BM];
   __shared__ double Bs[M][BK][BN];
@@ -124,27 +124,47 @@ __global__ void splitk_reduce_kernel(int64_t m, int64_t n, int64_t S, const doub
 
 
 // ---------------------------------------------------------------------------
-// GEMM launcher with split-K for long reductions
+// GEMM launcher: tile variant and split-K chosen from the shape so that small
+// and skinny products (panel-internal updates, W^T C with few rows) still fill
+// the 148 SMs; long reductions are split with a fixed-order partial reduction.
 // ---------------------------------------------------------------------------
+template <int M, int V, bool TA, bool TB>
+void gemm_launch(cudaStream_t st, int64_t m, int64_t n, int64_t k, CMat A, CMat B, Mat C, int mode, double* part,
+                 int64_t part_cap_elems) {
+  using Tl = GemmTile<M, V>;
+  const int64_t tiles = cdiv(m, Tl::BM) * cdiv(n, Tl::BN);
+  const int64_t target = 2 * kNumSMs;
+  int64_t S = 1;
+  if (part && tiles < target && k >= 4 * Tl::BK) {
+    S = std::min<int64_t>(kMaxSplitK, cdiv(target, tiles));
+    S = std::min<int64_t>(S, k / (2 * Tl::BK));
+    while (S > 1 && m * n * S > part_cap_elems) --S;
+    S = std::max<int64_t>(S, 1);
+  }
+  int64_t kc = cdiv(cdiv(k, S), Tl::BK) * Tl::BK;
+  S = std::max<int64_t>(1, cdiv(k, kc));
+  GemmArgs g{m, n, k, A.p, A.ld, A.ps, B.p, B.ld, B.ps, C.p, C.ld, C.ps, mode, kc, S > 1 ? part : nullptr, S};
+  dim3 grid((unsigned)cdiv(n, Tl::BN), (unsigned)cdiv(m, Tl::BM), (unsigned)S);
+  MDLS_LAUNCH(F_GEMM, st, gemm_kernel<M, V, TA, TB><<<grid, Tl::NT, 0, st>>>(g));
+  if (S > 1)
+    MDLS_LAUNCH(F_GEMM, st, splitk_reduce_kernel<M><<<grid_for(m * n, 256), 256, 0, st>>>(m, n, S, part, C.p, C.ld, C.ps, mode));
+}
+
 template <int M, bool TA, bool TB>
 void gemm(cudaStream_t st, int64_t m, int64_t n, int64_t k, CMat A, CMat B, Mat C, int mode, double* part,
           int64_t part_cap_elems) {
-  using Cfg = GemmCfg<M>;
-  constexpr int NT = (Cfg::BM / Cfg::TM) * (Cfg::BN / Cfg::TN);
   if (m <= 0 || n <= 0) return;
-  const int64_t tiles = cdiv(m, Cfg::BM) * cdiv(n, Cfg::BN);
-  int64_t S = 1;
-  if (part && k > 4 * Cfg::BK) {
-    S = std::min<int64_t>(kMaxSplit, std::max<int64_t>(1, (2 * kNumSMs) / tiles));
-    S = std::min<int64_t>(S, cdiv(k, 4 * Cfg::BK));
-    while (S > 1 && m * n * S > part_cap_elems) --S;
+  const int64_t target = 2 * kNumSMs;
+  if (m <= GemmTile<M, 2>::BM && n > m) {
+    gemm_launch<M, 2, TA, TB>(st, m, n, k, A, B, C, mode, part, part_cap_elems);
+  } else if (n <= GemmTile<M, 3>::BN && m > n) {
+    gemm_launch<M, 3, TA, TB>(st, m, n, k, A, B, C, mode, part, part_cap_elems);
+  } else {
+    const int64_t t0 = cdiv(m, GemmTile<M, 0>::BM) * cdiv(n, GemmTile<M, 0>::BN);
+    const bool can_split = part && k >= 8 * GemmTile<M, 0>::BK;
+    if (t0 >= target || (can_split && t0 >= target / 8)) gemm_launch<M, 0, TA, TB>(st, m, n, k, A, B, C, mode, part, part_cap_elems);
+    else gemm_launch<M, 1, TA, TB>(st, m, n, k, A, B, C, mode, part, part_cap_elems);
   }
-  int64_t kc = cdiv(cdiv(k, S), Cfg::BK) * Cfg::BK;
-  S = std::max<int64_t>(1, cdiv(k, kc));
-  GemmArgs g{m, n, k, A.p, A.ld, A.ps, B.p, B.ld, B.ps, C.p, C.ld, C.ps, mode, kc, S > 1 ? part : nullptr, S};
-  dim3 grid((unsigned)cdiv(n, Cfg::BN), (unsigned)cdiv(m, Cfg::BM), (unsigned)S);
-  MDLS_LAUNCH(F_GEMM, st, gemm_kernel<M, TA, TB><<<grid, NT, 0, st>>>(g));
-  if (S > 1) MDLS_LAUNCH(F_GEMM, st, splitk_reduce_kernel<M><<<grid_for(m * n, 256), 256, 0, st>>>(m, n, S, part, C.p, C.ld, C.ps, mode));
 }
 
 #define MDLS_INSTANTIATE_GEMM(MM, TA, TB)                                                                   \

@@ -1,0 +1,406 @@
+// kern_leaf.cuh -- A1 + A2 (and the sub-panel T of A3): Householder factorisation of a
+// narrow sub-panel ("leaf", B columns) by one thread-block cluster.
+//
+// Algorithm 2 step 1: for each column, compute v and beta (GVL Alg.
+// 5.1.1) and update the rest of the tile.  The tile (rows js..M-1,
+// columns js..js+B-1) is partitioned by rows over the C CTAs of a cluster and
+// held in shared memory for the whole leaf.  Per column ONE reduction suffices:
+// with x the current column below the pivot and v = x / v1 (v(1) = 1),
+//     v . a_c   = a_jc + (1/v1) * sum_{i>j} x_i a_ic          (beta R^T v)
+//     Y_c^T v   = y_jc + (1/v1) * sum_{i>j} x_i y_ic   (c < l, previous vectors)
+//     sigma     = sum_{i>j} x_i^2
+// so the B sums g_c = sum_{i>j} x_i t_ic over the whole tile row (t = a or y)
+// are reduced together: per-thread products, a warp reduce-scatter (halving),
+// a cross-warp smem sum, then one cluster barrier and a fixed-order DSMEM sum
+// over the C CTA partials.  Every CTA then computes the Householder scalars
+// redundantly (identical bits), updates its rows, and CTA 0 builds the leaf's
+// compact-WY factor T (T_ll = beta_l, T(:l, l) = -beta_l T(:l,:l) Y(:,:l)^T v_l,
+// which is the paper's z = -beta (v + W Y^T v), with W = -Y T).
+#pragma once
+#include "types.cuh"
+
+namespace mdls {
+
+template <int M>
+struct LeafArgs {
+  int64_t Mrows;  // rows of A
+  int64_t js;     // first column of the leaf (= first pivot row)
+  int64_t R;      // tile rows per CTA
+  Mat A;          // matrix (R and v written in place)
+  Mat Y;          // explicit Y store (same indexing as A)
+  double* beta;   // beta of global column j at beta[l*bps + j]
+  int64_t bps;
+  Mat T;          // B x B leaf T (upper triangular, zeros below)
+  int* info;      // min-slot: 1-based first zero / non-finite R_jj
+};
+
+// Reduce-scatter sum of V md values over the lanes of a warp that share
+// (lane % TPR): halving exchanges on the lane bits above TPR.  On return the
+// lane holds the full sums of values base..base+W_END-1 in v[0..W_END).
+// `plain` collects the lane bits of the levels that ended as plain pairwise
+// adds (lanes with those bits clear hold the canonical copy).
+template <int M, int W, int MASK, int TPR>
+struct HalveSum {
+  static constexpr int W_END = (MASK < TPR) ? W : HalveSum<M, (W > 1 ? W / 2 : 1), MASK / 2, TPR>::W_END;
+  __device__ __forceinline__ static void run(md<M>* v, int lane, int& base, int& plain) {
+    if constexpr (MASK >= TPR && MASK > 0) {
+      if constexpr (W > 1) {
+        constexpr int half = W / 2;
+        const bool up = (lane & MASK) != 0;
+#pragma unroll
+        for (int q = 0; q < half; ++q) {
+          md<M> send, keep;
+#pragma unroll
+          for (int k = 0; k < M; ++k) {
+            send.v[k] = up ? v[q].v[k] : v[q + half].v[k];
+            keep.v[k] = up ? v[q + half].v[k] : v[q].v[k];
+          }
+          v[q] = add<M>(keep, shfl_xor<M>(send, MASK));
+        }
+        if (up) base += half;
+        HalveSum<M, half, MASK / 2, TPR>::run(v, lane, base, plain);
+      } else {
+        v[0] = add<M>(v[0], shfl_xor<M>(v[0], MASK));
+        plain |= MASK;
+        HalveSum<M, 1, MASK / 2, TPR>::run(v, lane, base, plain);
+      }
+    }
+  }
+};
+template <int M, int W, int TPR>
+struct HalveSum<M, W, 0, TPR> {
+  static constexpr int W_END = W;
+  __device__ __forceinline__ static void run(md<M>*, int, int&, int&) {}
+};
+
+// Householder scalars (GVL Alg. 5.1.1): from sigma and x1, mu = sqrt(x1^2 +
+// sigma), v1 = x1 - mu (x1 <= 0) or -sigma / (x1 + mu).  sigma = 0: P = I.
+template <int M>
+__device__ __noinline__ void house_v1(const md<M>& sigma, const md<M>& x1, md<M>& mu, md<M>& v1) {
+  mu = sqrt<M>(add<M>(mul<M>(x1, x1), sigma));
+  if (x1.v[0] <= 0.0) v1 = sub<M>(x1, mu);
+  else v1 = div<M>(neg(sigma), add<M>(x1, mu));
+}
+// beta = 2 v1^2 / (sigma + v1^2)
+template <int M>
+__device__ __noinline__ md<M> house_beta(const md<M>& sigma, const md<M>& v1) {
+  const md<M> v1sq = mul<M>(v1, v1);
+  return div<M>(scale_pow2<M>(v1sq, 2.0), add<M>(sigma, v1sq));
+}
+template <int M>
+__device__ __noinline__ md<M> md_recip(const md<M>& v1) {
+  return div<M>(md_from<M>(1.0), v1);
+}
+
+template <int M, int B, int TPR, int NT>
+__global__ void __launch_bounds__(NT) leaf_kernel(LeafArgs<M> a) {
+  constexpr int V = B / TPR;      // tile columns per thread
+  constexpr int NW = NT / 32;     // warps
+  constexpr int NRG = NT / TPR;   // row groups
+  constexpr int GS = (NT / B >= 32) ? 32 : (NT / B >= 16 ? 16 : (NT / B >= 8 ? 8 : (NT / B >= 4 ? 4 : (NT / B >= 2 ? 2 : 1))));
+  static_assert(V >= 1 && B % TPR == 0, "leaf shape");
+  static_assert(NT % B == 0 || B > NT, "leaf threads");
+
+  cg::cluster_group cluster = cg::this_cluster();
+  const int C = (int)cluster.num_blocks();
+  const int rank = (int)cluster.block_rank();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int h = tid % TPR, rg = tid / TPR;
+
+  extern __shared__ double smem_leaf[];
+  const int64_t R = a.R;
+  double* tile = smem_leaf;                       // [M][B][R]
+  double* vsm = smem_leaf + (int64_t)M * B * R;   // [M][R]
+  __shared__ md<M> wpart[NW][B];
+  __shared__ md<M> red[2][B];
+  __shared__ md<M> piv[2][B];
+  __shared__ md<M> G[B], pv[B], wv[B], betas[B];
+  __shared__ md<M> SY[B][B];  // SY[p][l] = Y_p^T v_l (p < l)
+  __shared__ md<M> Ts[B][B];  // leaf T, Ts[row][col]
+  __shared__ md<M> sc_mu, sc_v1, sc_beta, sc_rv1;
+  __shared__ int sc_deg;
+
+  auto T_ = [&](int64_t i, int c, int l) -> double& { return tile[((int64_t)l * B + c) * R + i]; };
+
+  const int64_t total = a.Mrows - a.js;
+  const int64_t row0 = a.js + (int64_t)rank * R;
+  int64_t Rp = total - (int64_t)rank * R;
+  Rp = Rp < 0 ? 0 : (Rp > R ? R : Rp);
+
+  // ---- load the tile ----
+  for (int64_t e = tid; e < Rp * B; e += NT) {
+    const int64_t i = e % Rp;
+    const int c = (int)(e / Rp);
+#pragma unroll
+    for (int l = 0; l < M; ++l) T_(i, c, l) = a.A.p[l * a.A.ps + (a.js + c) * a.A.ld + row0 + i];
+  }
+  __syncthreads();
+
+  for (int l = 0; l < B; ++l) {
+    const int64_t j = a.js + l;
+    const int buf = l & 1;
+    const int64_t pr_abs = j - a.js;
+    const int p_piv = (int)(pr_abs / R);
+    const int64_t pr = pr_abs - (int64_t)p_piv * R;
+
+    // (1) per-thread products x_i * t_ic over own rows below the pivot
+    md<M> acc[V];
+#pragma unroll
+    for (int q = 0; q < V; ++q) acc[q] = md_zero<M>();
+    for (int64_t i = rg; i < Rp; i += NRG) {
+      if (row0 + i <= j) continue;
+      md<M> x;
+#pragma unroll
+      for (int k = 0; k < M; ++k) x.v[k] = T_(i, l, k);
+#pragma unroll
+      for (int q = 0; q < V; ++q) {
+        md<M> t;
+#pragma unroll
+        for (int k = 0; k < M; ++k) t.v[k] = T_(i, h * V + q, k);
+        acc[q] = fma<M>(acc[q], x, t);
+      }
+    }
+    // (2) warp reduce-scatter, (3) cross-warp sum -> CTA partial
+    int base = 0, plain = 0;
+    HalveSum<M, V, 16, TPR>::run(acc, lane, base, plain);
+    constexpr int WE = HalveSum<M, V, 16, TPR>::W_END;
+    if ((lane & plain) == 0) {
+#pragma unroll
+      for (int q = 0; q < WE; ++q) wpart[warp][h * V + base + q] = acc[q];
+    }
+    __syncthreads();
+    if (tid < B) {
+      md<M> s = wpart[0][tid];
+      for (int w = 1; w < NW; ++w) s = add<M>(s, wpart[w][tid]);
+      red[buf][tid] = s;
+      if (rank == p_piv) {
+        md<M> pvv;
+#pragma unroll
+        for (int k = 0; k < M; ++k) pvv.v[k] = T_(pr, tid, k);
+        piv[buf][tid] = pvv;
+      }
+    }
+    cluster.sync();
+
+    // (4) fixed-order sum of the C partials (DSMEM), pivot row from its owner
+    if (tid < B * GS) {
+      const int c = tid / GS, sub = tid % GS;
+      md<M> s = md_zero<M>();
+      bool have = false;
+      for (int q = sub; q < C; q += GS) {
+        const md<M>* rp = cluster.map_shared_rank(&red[buf][c], q);
+        md<M> t = *rp;
+        s = have ? add<M>(s, t) : t;
+        have = true;
+      }
+#pragma unroll
+      for (int d = GS / 2; d >= 1; d >>= 1) {
+        md<M> o = shfl_down<M>(s, d);
+        if (sub + d < GS && sub + d < C) s = add<M>(s, o);  // lanes beyond C hold nothing
+      }
+      if (sub == 0) {
+        G[c] = s;
+        pv[c] = *cluster.map_shared_rank(&piv[buf][c], p_piv);
+      }
+    }
+    __syncthreads();
+
+    // (5) Householder scalars (every CTA, identical); CTA 0 builds T column l-1 meanwhile
+    if (tid == 0) {
+      const md<M> sigma = G[l], x1 = pv[l];
+      if (sigma.v[0] == 0.0) {
+        sc_deg = 1;
+        sc_mu = x1;
+        sc_v1 = md_from<M>(1.0);
+      } else {
+        sc_deg = 0;
+        md<M> mu, v1;
+        house_v1<M>(sigma, x1, mu, v1);
+        sc_mu = mu;
+        sc_v1 = v1;
+      }
+    } else if (rank == 0 && warp == NW - 1 && l > 0) {
+      // T(:, l-1): T(ll, ll) = beta_ll; T(r, ll) = -beta_ll * sum_{p=r}^{ll-1} T(r, p) SY[p][ll]
+      const int ll = l - 1, r = lane;
+      if (r < ll) {
+        md<M> s = md_zero<M>();
+        for (int p = r; p < ll; ++p) s = fma<M>(s, Ts[r][p], SY[p][ll]);
+        Ts[r][ll] = neg(mul<M>(betas[ll], s));
+      } else if (r == ll) {
+        Ts[ll][ll] = betas[ll];
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      sc_beta = sc_deg ? md_zero<M>() : house_beta<M>(G[l], sc_v1);
+    } else if (tid == 32 % NT) {
+      sc_rv1 = sc_deg ? md_from<M>(1.0) : md_recip<M>(sc_v1);
+    }
+    __syncthreads();
+    const md<M> beta = sc_beta, rv1 = sc_rv1;
+    const int deg = sc_deg;
+    // (6) w_c = beta (a_jc + rv1 g_c) for c > l; Y_c^T v = y_jc + rv1 g_c for c < l
+    if (tid < B) {
+      const int c = tid;
+      if (c != l) {
+        const md<M> t = deg ? pv[c] : add<M>(pv[c], mul<M>(rv1, G[c]));
+        if (c > l) wv[c] = mul<M>(beta, t);
+        else SY[c][l] = t;
+      } else {
+        betas[l] = beta;
+      }
+    }
+    // v below the pivot (owner threads of column l)
+    if (h == l / V) {
+      for (int64_t i = rg; i < Rp; i += NRG) {
+        if (row0 + i <= j) continue;
+        md<M> x;
+#pragma unroll
+        for (int k = 0; k < M; ++k) x.v[k] = T_(i, l, k);
+        const md<M> v = deg ? x : mul<M>(x, rv1);
+#pragma unroll
+        for (int k = 0; k < M; ++k) vsm[(int64_t)k * R + i] = v.v[k];
+      }
+    }
+    __syncthreads();
+    // (7) update own rows: t_ic -= v_i w_c (c > l); column l <- v (R_jj = mu on the pivot row)
+    for (int64_t i = rg; i < Rp; i += NRG) {
+      const int64_t gi = row0 + i;
+      if (gi < j) continue;
+      md<M> v;
+      if (gi == j) {
+        v = md_from<M>(1.0);
+      } else {
+#pragma unroll
+        for (int k = 0; k < M; ++k) v.v[k] = vsm[(int64_t)k * R + i];
+      }
+#pragma unroll
+      for (int q = 0; q < V; ++q) {
+        const int c = h * V + q;
+        if (c > l) {
+          md<M> t;
+#pragma unroll
+          for (int k = 0; k < M; ++k) t.v[k] = T_(i, c, k);
+          t = (gi == j) ? add<M>(t, neg(wv[c])) : fms<M>(t, v, wv[c]);
+#pragma unroll
+          for (int k = 0; k < M; ++k) T_(i, c, k) = t.v[k];
+        } else if (c == l) {
+          const md<M> out = (gi == j) ? sc_mu : v;
+#pragma unroll
+          for (int k = 0; k < M; ++k) T_(i, c, k) = out.v[k];
+        }
+      }
+    }
+    if (tid == 0 && rank == 0) {
+      const double m0 = sc_mu.v[0];
+      if (!(m0 != 0.0) || !isfinite(m0)) atomicMin(a.info, (int)(j + 1));
+    }
+    __syncthreads();
+  }
+
+  // ---- last T column, write-back of R/v, explicit Y, beta, T ----
+  if (rank == 0 && warp == NW - 1) {
+    const int ll = B - 1, r = lane;
+    if (r < ll) {
+      md<M> s = md_zero<M>();
+      for (int p = r; p < ll; ++p) s = fma<M>(s, Ts[r][p], SY[p][ll]);
+      Ts[r][ll] = neg(mul<M>(betas[ll], s));
+    } else if (r == ll) {
+      Ts[ll][ll] = betas[ll];
+    }
+  }
+  for (int64_t e = tid; e < Rp * B; e += NT) {
+    const int64_t i = e % Rp;
+    const int c = (int)(e / Rp);
+    const int64_t gi = row0 + i, jc = a.js + c;
+#pragma unroll
+    for (int l = 0; l < M; ++l) {
+      const double t = T_(i, c, l);
+      a.A.p[l * a.A.ps + jc * a.A.ld + gi] = t;
+      a.Y.p[l * a.Y.ps + jc * a.Y.ld + gi] = (gi < jc) ? 0.0 : (gi == jc ? (l == 0 ? 1.0 : 0.0) : t);
+    }
+  }
+  __syncthreads();
+  if (rank == 0) {
+    if (tid < B) st<M>(a.beta, a.bps, a.js + tid, betas[tid]);
+    for (int e = tid; e < B * B; e += NT) {
+      const int r = e % B, c = e / B;
+      st<M>(a.T.p, a.T.ps, r + (int64_t)c * a.T.ld, (r <= c) ? Ts[r][c] : md_zero<M>());
+    }
+  }
+  cluster.sync();  // keep every CTA's shared memory alive until all DSMEM reads are done
+}
+
+// ---------------------------------------------------------------------------
+// launcher: cluster size C (16, non-portable; 8 fallback), leaf width B
+// (power of two dividing nb, capped per precision and by shared memory)
+// ---------------------------------------------------------------------------
+template <int M, int B, int TPR>
+cudaError_t leaf_launch_impl(cudaStream_t st, const LeafArgs<M>& la, int C) {
+  constexpr int NT = 128;
+  auto kern = leaf_kernel<M, B, TPR, NT>;
+  const size_t smem = sizeof(double) * (size_t)M * (B + 1) * la.R;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C, 1, 1);
+  cfg.blockDim = dim3(NT, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  trace_begin(st, F_PANEL);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, la);
+  trace_end(st, F_PANEL);
+  return e;
+}
+
+inline size_t leaf_smem_bytes(int M, int B, int64_t R) { return sizeof(double) * (size_t)M * (B + 1) * R; }
+
+// factor columns [js, js+B) of A (rows js..Mrows-1); returns B used via *bw
+template <int M>
+cudaError_t launch_leaf(cudaStream_t st, int64_t Mrows, int64_t js, int64_t bmax, Mat A, Mat Y, double* beta,
+                        int64_t bps, Mat T, int* info, int* bw) {
+  static int csize = 16;
+  const int64_t rows = Mrows - js;
+  const size_t cap = 200 * 1024;
+  int B = 1;
+  while (B * 2 <= bmax && B * 2 <= (M == 2 ? 16 : 8)) B *= 2;
+  for (;;) {
+    const int C = (int)std::max<int64_t>(1, std::min<int64_t>(csize, rows));
+    const int64_t R = cdiv(rows, C);
+    while (B > 1 && leaf_smem_bytes(M, B, R) > cap) B /= 2;
+    if (leaf_smem_bytes(M, B, R) > cap) return cudaErrorInvalidValue;
+    LeafArgs<M> la{Mrows, js, R, A, Y, beta, bps, T, info};
+    cudaError_t e;
+    switch (B) {
+      case 16:
+        if constexpr (M == 2) {
+          e = leaf_launch_impl<M, 16, 2>(st, la, C);
+          break;
+        }
+        [[fallthrough]];
+      case 8: e = leaf_launch_impl<M, 8, 2>(st, la, C); break;
+      case 4: e = leaf_launch_impl<M, 4, 2>(st, la, C); break;
+      case 2: e = leaf_launch_impl<M, 2, 2>(st, la, C); break;
+      default: e = leaf_launch_impl<M, 1, 1>(st, la, C); break;
+    }
+    if (e == cudaSuccess || csize == 8) {
+      *bw = B;
+      return e;
+    }
+    cudaGetLastError();
+    csize = 8;  // non-portable cluster size refused: fall back to 8
+  }
+}
+
+#define MDLS_INSTANTIATE_LEAF(MM)                                                                               \
+  template cudaError_t launch_leaf<MM>(cudaStream_t, int64_t, int64_t, int64_t, Mat, Mat, double*, int64_t, Mat, \
+                                       int*, int*);
+
+}  // namespace mdls

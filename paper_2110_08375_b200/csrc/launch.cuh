@@ -11,7 +11,8 @@ void gemm(cudaStream_t st, int64_t m, int64_t n, int64_t k, CMat A, CMat B, Mat 
           int64_t part_cap_elems);
 
 template <int M>
-cudaError_t launch_panel(cudaStream_t st, const PanelArgs<M>& pa);
+cudaError_t launch_leaf(cudaStream_t st, int64_t Mrows, int64_t js, int64_t bmax, Mat A, Mat Y, double* beta,
+                        int64_t bps, Mat T, int* info, int* bw);
 
 template <int M>
 void launch_invert(cudaStream_t st, int64_t ntiles, int64_t nb, CMat U, Mat Vt, double diag_scale, const double* dbeta,

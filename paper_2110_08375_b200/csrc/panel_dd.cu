@@ -1,5 +1,5 @@
-// panel-factorisation instantiation for dd (2 limbs).
-#include "kern_panel.cuh"
+// leaf (sub-panel) factorisation instantiation for dd (2 limbs).
+#include "kern_leaf.cuh"
 namespace mdls {
-MDLS_INSTANTIATE_PANEL(2)
+MDLS_INSTANTIATE_LEAF(2)
 }  // namespace mdls

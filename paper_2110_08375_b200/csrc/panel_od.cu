@@ -1,5 +1,5 @@
-// panel-factorisation instantiation for od (8 limbs).
-#include "kern_panel.cuh"
+// leaf (sub-panel) factorisation instantiation for od (8 limbs).
+#include "kern_leaf.cuh"
 namespace mdls {
-MDLS_INSTANTIATE_PANEL(8)
+MDLS_INSTANTIATE_LEAF(8)
 }  // namespace mdls

@@ -1,5 +1,5 @@
-// panel-factorisation instantiation for qd (4 limbs).
-#include "kern_panel.cuh"
+// leaf (sub-panel) factorisation instantiation for qd (4 limbs).
+#include "kern_leaf.cuh"
 namespace mdls {
-MDLS_INSTANTIATE_PANEL(4)
+MDLS_INSTANTIATE_LEAF(4)
 }  // namespace mdls

@@ -44,7 +44,7 @@ Plan make_plan(int op, int64_t Mr, int64_t K, int64_t nb) {
     p.w = take(md * Mr * K);
     p.beta = take(md * K);
     p.s = take(md * nb * nb);
-    p.t = take(md * nb * nb);
+    p.t = take(md * std::max<int64_t>(nb * nb, 256));
   }
   if (op == MDLS_OP_APPLY_QT) p.y = take(md * Mr * K);
   if (qr_like || op == MDLS_OP_APPLY_QT) {
@@ -74,42 +74,68 @@ struct QrBufs {
   int* info_slot;
 };
 
-// factor panels [kbeg, kend) and build their W (P_WY = I + W Y^T, P:495-512;
-// W = -Y T with T^-1 = striu(Y^T Y) + diag(Y^T Y)/2 -- DESIGN.md "WY build"),
-// applying each panel to the trailing columns when `trailing`
+// Panel k of Algorithm 2: factor columns [j0, j0+nb) in leaves of
+// B <= 16 columns (launch_leaf: v, beta, R, leaf T); after each leaf
+//   W_s = -Y_s T_s                              (the leaf's P_WY = I + W_s Y_s^T)
+//   C_s += Y_s (W_s^T C_s)  on the panel columns right of the leaf ("beta R^T v",
+//                                                 "update R" as two md GEMMs)
+//   W_s += W_<s (Y_<s^T W_s) (block form of z = -beta (v + W Y^T v))
+// so the panel's W (P_WY = I + W Y^T) is built column block by block.
+template <int M>
+cudaError_t qr_panel(cudaStream_t st, int64_t Mr, int64_t nb, int64_t k, Mat A, Mat Y, Mat W, double* beta,
+                     int64_t bps, const QrBufs<M>& b) {
+  const int64_t j0 = k * nb, r = Mr - j0;
+  int64_t js = j0;
+  while (js < j0 + nb) {
+    int bw = 1;
+    set_stage(MDLS_ST_PANEL);
+    Mat Tl{b.T.p, 16, 256};
+    cudaError_t e = launch_leaf<M>(st, Mr, js, j0 + nb - js, A, Y, beta, bps, Tl, b.info_slot, &bw);
+    if (e != cudaSuccess) return e;
+    const int64_t rs = Mr - js;
+    const CMat Ys = sub(cm(Y), js, js);
+    Mat Ws = sub(W, js, js);
+    set_stage(MDLS_ST_WY);
+    gemm<M, false, false>(st, rs, bw, bw, Ys, cm(Tl), Ws, 3, nullptr, 0);  // W_s = -Y_s T_s
+    const int64_t rem = j0 + nb - (js + bw);
+    if (rem > 0) {
+      set_stage(MDLS_ST_PANEL);
+      Mat Cs = sub(A, js, js + bw);
+      gemm<M, true, false>(st, bw, rem, rs, cm(Ws), cm(Cs), b.X, 0, b.part, b.part_cap);
+      gemm<M, false, false>(st, rs, rem, bw, Ys, cm(b.X), Cs, 1, nullptr, 0);
+    }
+    if (js > j0) {
+      set_stage(MDLS_ST_WY);
+      const int64_t np = js - j0;
+      gemm<M, true, false>(st, np, bw, rs, sub(cm(Y), js, j0), cm(Ws), b.X, 0, b.part, b.part_cap);
+      gemm<M, false, false>(st, r, bw, np, sub(cm(W), j0, j0), cm(b.X), sub(W, j0, js), 1, nullptr, 0);
+    }
+    js += bw;
+  }
+  (void)r;
+  return cudaGetLastError();
+}
+
+// apply panel k to the columns [c0, c1) of A: C += Y_k (W_k^T C) ("YWT * C", "R + YWTC")
+template <int M>
+void qr_apply_panel(cudaStream_t st, int64_t Mr, int64_t nb, int64_t k, CMat Yk, CMat Wk, Mat A, int64_t c0,
+                    int64_t c1, const QrBufs<M>& b) {
+  if (c1 <= c0) return;
+  const int64_t j0 = k * nb, r = Mr - j0;
+  set_stage(MDLS_ST_TRAILING);
+  Mat Cm = sub(A, j0, c0);
+  gemm<M, true, false>(st, nb, c1 - c0, r, Wk, cm(Cm), b.X, 0, b.part, b.part_cap);
+  gemm<M, false, false>(st, r, c1 - c0, nb, Yk, cm(b.X), Cm, 1, nullptr, 0);
+}
+
 template <int M>
 cudaError_t qr_factor(cudaStream_t st, int64_t Mr, int64_t K, int64_t nb, Mat A, const QrBufs<M>& b, int64_t kbeg,
                       int64_t kend, bool trailing) {
   for (int64_t k = kbeg; k < kend; ++k) {
-    const int64_t j0 = k * nb, r = Mr - j0, c = K - j0 - nb;
-    PanelArgs<M> pa;
-    pa.Mrows = Mr;
-    pa.j0 = j0;
-    pa.w = nb;
-    pa.A = A;
-    pa.Y = b.Y;
-    pa.beta = b.beta;
-    pa.bps = K;
-    pa.info = b.info_slot;
-    set_stage(MDLS_ST_PANEL);
-    cudaError_t e = launch_panel<M>(st, pa);
+    const int64_t j0 = k * nb;
+    cudaError_t e = qr_panel<M>(st, Mr, nb, k, A, b.Y, b.W, b.beta, K, b);
     if (e != cudaSuccess) return e;
-    const CMat Yp = sub(cm(b.Y), j0, j0);
-    // S = Yp^T Yp (nb x nb)
-    set_stage(MDLS_ST_WY);
-    gemm<M, true, false>(st, nb, nb, r, Yp, Yp, b.S, 0, b.part, b.part_cap);
-    // T = inv(striu(S) + diag(S)/2), stored transposed in b.T
-    launch_invert<M>(st, 1, nb, cm(b.S), b.T, 0.5, b.beta + j0, b.info_slot + 1);
-    // W_p = -Y_p T  (T^T stored => TB)
-    gemm<M, false, true>(st, r, nb, nb, Yp, cm(b.T), sub(b.W, j0, j0), 3, nullptr, 0);
-    if (trailing && c > 0) {
-      set_stage(MDLS_ST_TRAILING);
-      const CMat Wp = sub(cm(b.W), j0, j0);
-      Mat Cm = sub(A, j0, j0 + nb);
-      // X = W_p^T C  ("YWT * C" first half), then C += Y_p X ("R + YWTC")
-      gemm<M, true, false>(st, nb, c, r, Wp, cm(Cm), b.X, 0, b.part, b.part_cap);
-      gemm<M, false, false>(st, r, c, nb, Yp, cm(b.X), Cm, 1, nullptr, 0);
-    }
+    if (trailing) qr_apply_panel<M>(st, Mr, nb, k, sub(cm(b.Y), j0, j0), sub(cm(b.W), j0, j0), A, j0 + nb, K, b);
   }
   return cudaGetLastError();
 }

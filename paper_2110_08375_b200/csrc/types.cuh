@@ -62,20 +62,28 @@ inline CMat cm(const Mat& a) { return CMat{a.p, a.ld, a.ps}; }
 inline Mat sub(const Mat& a, int64_t i, int64_t j) { return Mat{a.p + i + j * a.ld, a.ld, a.ps}; }
 inline CMat sub(const CMat& a, int64_t i, int64_t j) { return CMat{a.p + i + j * a.ld, a.ld, a.ps}; }
 
-template <int M>
-struct GemmCfg;
-template <>
-struct GemmCfg<2> {
-  static constexpr int BM = 64, BN = 64, BK = 16, TM = 4, TN = 4;
+// md GEMM tile variants: <BM, BN, BK, TM, TN>; V = 0 large, 1 medium, 2 skinny-m
+// (few output rows, e.g. W^T C), 3 skinny-n (few output columns, e.g. Q^T b)
+template <int BM_, int BN_, int BK_, int TM_, int TN_>
+struct Tile {
+  static constexpr int BM = BM_, BN = BN_, BK = BK_, TM = TM_, TN = TN_;
+  static constexpr int NT = (BM / TM) * (BN / TN);
 };
-template <>
-struct GemmCfg<4> {
-  static constexpr int BM = 32, BN = 32, BK = 16, TM = 2, TN = 2;
-};
-template <>
-struct GemmCfg<8> {
-  static constexpr int BM = 16, BN = 16, BK = 16, TM = 1, TN = 1;
-};
+template <int M, int V>
+struct GemmTile;
+template <> struct GemmTile<2, 0> : Tile<64, 64, 16, 4, 4> {};
+template <> struct GemmTile<2, 1> : Tile<32, 32, 16, 2, 2> {};
+template <> struct GemmTile<2, 2> : Tile<16, 64, 16, 1, 4> {};
+template <> struct GemmTile<2, 3> : Tile<64, 16, 16, 4, 1> {};
+template <> struct GemmTile<4, 0> : Tile<32, 32, 16, 2, 2> {};
+template <> struct GemmTile<4, 1> : Tile<16, 16, 16, 1, 1> {};
+template <> struct GemmTile<4, 2> : Tile<16, 32, 16, 1, 2> {};
+template <> struct GemmTile<4, 3> : Tile<32, 16, 16, 2, 1> {};
+template <> struct GemmTile<8, 0> : Tile<32, 16, 16, 2, 1> {};
+template <> struct GemmTile<8, 1> : Tile<16, 16, 16, 1, 1> {};
+template <> struct GemmTile<8, 2> : Tile<8, 32, 16, 1, 1> {};
+template <> struct GemmTile<8, 3> : Tile<32, 8, 16, 1, 1> {};
+constexpr int64_t kMaxSplitK = 64;
 
 struct GemmArgs {
   int64_t m, n, k;
@@ -91,14 +99,5 @@ struct GemmArgs {
   int64_t S;      // number of splits
 };
 
-template <int M>
-struct PanelArgs {
-  int64_t Mrows, j0, w;
-  Mat A;
-  Mat Y;          // explicit Y (same row/column indexing as A)
-  double* beta;   // beta of global column j at beta[l*bps + j]
-  int64_t bps;
-  int* info;      // min-slot: 1-based first zero/non-finite R_jj
-};
 
 }  // namespace mdls
