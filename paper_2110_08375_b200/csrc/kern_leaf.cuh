@@ -92,6 +92,14 @@ __device__ __noinline__ md<M> md_recip(const md<M>& v1) {
   return div<M>(md_from<M>(1.0), v1);
 }
 
+#ifdef MDLS_LEAF_PROF
+__device__ long long g_leaf_prof[64 * 12];
+#define LEAF_MARK(l, ph) \
+  if (rank == 0 && tid == 0 && (l) < 64) g_leaf_prof[(l) * 12 + (ph)] = clock64();
+#else
+#define LEAF_MARK(l, ph)
+#endif
+
 template <int M, int B, int TPR, int NT>
 __global__ void __launch_bounds__(NT) leaf_kernel(LeafArgs<M> a) {
   constexpr int V = B / TPR;      // tile columns per thread
@@ -143,6 +151,7 @@ __global__ void __launch_bounds__(NT) leaf_kernel(LeafArgs<M> a) {
     const int p_piv = (int)(pr_abs / R);
     const int64_t pr = pr_abs - (int64_t)p_piv * R;
 
+    LEAF_MARK(l, 0);
     // (1) per-thread products x_i * t_ic over own rows below the pivot
     md<M> acc[V];
 #pragma unroll
@@ -160,6 +169,7 @@ __global__ void __launch_bounds__(NT) leaf_kernel(LeafArgs<M> a) {
         acc[q] = fma<M>(acc[q], x, t);
       }
     }
+    LEAF_MARK(l, 1);
     // (2) warp reduce-scatter, (3) cross-warp sum -> CTA partial
     int base = 0, plain = 0;
     HalveSum<M, V, 16, TPR>::run(acc, lane, base, plain);
@@ -180,7 +190,9 @@ __global__ void __launch_bounds__(NT) leaf_kernel(LeafArgs<M> a) {
         piv[buf][tid] = pvv;
       }
     }
+    LEAF_MARK(l, 2);
     cluster.sync();
+    LEAF_MARK(l, 3);
 
     // (4) fixed-order sum of the C partials (DSMEM), pivot row from its owner
     if (tid < B * GS) {
@@ -204,6 +216,7 @@ __global__ void __launch_bounds__(NT) leaf_kernel(LeafArgs<M> a) {
       }
     }
     __syncthreads();
+    LEAF_MARK(l, 4);
 
     // (5) Householder scalars (every CTA, identical); CTA 0 builds T column l-1 meanwhile
     if (tid == 0) {
@@ -231,12 +244,14 @@ __global__ void __launch_bounds__(NT) leaf_kernel(LeafArgs<M> a) {
       }
     }
     __syncthreads();
+    LEAF_MARK(l, 5);
     if (tid == 0) {
       sc_beta = sc_deg ? md_zero<M>() : house_beta<M>(G[l], sc_v1);
     } else if (tid == 32 % NT) {
       sc_rv1 = sc_deg ? md_from<M>(1.0) : md_recip<M>(sc_v1);
     }
     __syncthreads();
+    LEAF_MARK(l, 6);
     const md<M> beta = sc_beta, rv1 = sc_rv1;
     const int deg = sc_deg;
     // (6) w_c = beta (a_jc + rv1 g_c) for c > l; Y_c^T v = y_jc + rv1 g_c for c < l
@@ -263,6 +278,7 @@ __global__ void __launch_bounds__(NT) leaf_kernel(LeafArgs<M> a) {
       }
     }
     __syncthreads();
+    LEAF_MARK(l, 7);
     // (7) update own rows: t_ic -= v_i w_c (c > l); column l <- v (R_jj = mu on the pivot row)
     for (int64_t i = rg; i < Rp; i += NRG) {
       const int64_t gi = row0 + i;
@@ -296,6 +312,7 @@ __global__ void __launch_bounds__(NT) leaf_kernel(LeafArgs<M> a) {
       if (!(m0 != 0.0) || !isfinite(m0)) atomicMin(a.info, (int)(j + 1));
     }
     __syncthreads();
+    LEAF_MARK(l, 8);
   }
 
   // ---- last T column, write-back of R/v, explicit Y, beta, T ----

@@ -168,3 +168,41 @@ def sharded_form_q(st: ShardState, W, Y, ops: Ops, new_empty, local_ranks):
             # exchanged roles: C += W_k (Y_k^T C)
             ops.update(st.prec, Y[k], W[k], Q[r], k, st.nb, first, len(cols))
     return Q
+
+
+def gather_columns(st: ShardState, pieces: dict, cols_of, comm: Comm | None, total: int, new_empty):
+    """Assemble a (m, total, L) array from per-rank column pieces (all ranks get it)."""
+    import torch
+
+    ranks = range(st.P)
+    some = next(iter(pieces.values()))
+    m, L = some.shape[0], some.shape[2]
+    if comm is not None:
+        sizes = [len(cols_of(st, r)) for r in ranks]
+        pad = new_empty((m, max(sizes), L))
+        mine = pieces[comm.rank]
+        pad[:, :mine.shape[1]] = mine
+        parts = comm.all_gather(pad)
+        pieces = {r: parts[r][:, :sizes[r]] for r in ranks}
+    out = new_empty((m, total, L))
+    for r, t in pieces.items():
+        idx = torch.tensor(cols_of(st, r), dtype=torch.long, device=t.device)
+        out[:, idx] = t
+    return out
+
+
+def sharded_lstsq(prec: str, A_loc: dict, b, M: int, K: int, nb: int, P: int, ops: Ops, comm: Comm | None,
+                  new_empty):
+    """x = argmin ||b - A x|| with A column-sharded over P ranks (A_loc[r] holds the
+    columns local_columns(st, r)).  Every rank returns the same x (and R, y)."""
+    st = plan(prec, M, K, nb, P)
+    W, Y = sharded_qr(st, A_loc, ops, comm, new_empty)
+    local = sorted(A_loc)
+    Q = sharded_form_q(st, W, Y, ops, new_empty, local)
+    # Q^T b: own column blocks, then all-gather the slices (byte movement)
+    ysl = {r: ops.qt_b_cols(prec, Q[r], b)[:, :, None] for r in local}
+    y = gather_columns(st, ysl, local_q_columns, comm, M, new_empty)[:, :, 0].contiguous()
+    # R: all-gather the factored panels, back substitution on the leading K x K
+    F = gather_columns(st, {r: A_loc[r] for r in local}, local_columns, comm, K, new_empty).contiguous()
+    x, info = ops.backsub(prec, F, y, nb)
+    return x, F, y, info
