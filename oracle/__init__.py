@@ -76,6 +76,7 @@ def _load(counting: bool = False) -> ctypes.CDLL:
     lib.oracle_inv_recon.restype = ctypes.c_double
     lib.oracle_inv_normal.argtypes = [ctypes.c_int, _I64, _I64, _D, _I64, _D, _D, ctypes.c_int]
     lib.oracle_inv_normal.restype = ctypes.c_double
+    lib.oracle_dot.argtypes = [ctypes.c_int, _I64, _D, _I64, _I64, _D, _I64, _I64, _D]
     lib.oracle_count_get.argtypes = [ctypes.POINTER(ctypes.c_uint64)]
     lib.oracle_selfcheck.restype = ctypes.c_int
     if lib.oracle_selfcheck() != 0:
@@ -279,3 +280,14 @@ def inv_normal(prec, A: np.ndarray, x: np.ndarray, b: np.ndarray, nthreads: int 
     _, K, M = A.shape
     return _load().oracle_inv_normal(m, M, K, _p(A), M, _p(np.ascontiguousarray(x)), _p(np.ascontiguousarray(b)),
                                      nthreads or default_threads())
+
+
+def dot(prec, a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """md dot product of two (m, n) md vectors (ascending accumulation)."""
+    m = _m_of(prec)
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    n = a.shape[1]
+    out = np.zeros(m)
+    _load().oracle_dot(m, n, _p(a), n, 1, _p(b), n, 1, _p(out))
+    return out

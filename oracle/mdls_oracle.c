@@ -636,6 +636,25 @@ int oracle_backsub(int m, int64_t n, const double *Rp, int64_t ldr, int64_t rcol
   return info;
 }
 
+/* md dot product s = sum_i a_i b_i accumulated from 0 in ascending i (n entries,
+ * planes pa / pb apart, strides sa / sb between entries) */
+int oracle_dot(int m, int64_t n, const double *a, int64_t pa, int64_t sa, const double *b, int64_t pb, int64_t sb,
+               double *out) {
+  if (m != 2 && m != 4 && m != 8) return -2;
+  double s[MAXM], t[MAXM], x[MAXM], y[MAXM];
+  md_zero(m, s);
+  for (int64_t i = 0; i < n; ++i) {
+    for (int k = 0; k < m; ++k) {
+      x[k] = a[k * pa + i * sa];
+      y[k] = b[k * pb + i * sb];
+    }
+    md_mul(m, x, y, t);
+    md_add(m, s, t, s);
+  }
+  md_copy(m, s, out);
+  return 0;
+}
+
 /* ------------------------------------------------------------------------- */
 /* least squares: A = QR (A copied), y = Q^T b (reflectors), R x = y(1:K)      */
 /* ------------------------------------------------------------------------- */

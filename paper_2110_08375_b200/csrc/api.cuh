@@ -2,6 +2,8 @@
 // Included by api_dd.cu / api_qd.cu / api_od.cu with MDLS_P (dd|qd|od) and
 // MDLS_M (2|4|8) defined; argument checking, workspace carving, launches.
 #pragma once
+#include <cstdlib>
+
 #include "solver.cuh"
 
 #define MDLS_CAT2(a, b) a##b
@@ -24,6 +26,22 @@ inline T* at(void* work, size_t off) {
 // plane strides must cover the operand
 inline bool mat_ok(const void* p, int64_t rows, int64_t cols, int64_t ld, int64_t ps) {
   return p && ld >= std::max<int64_t>(1, rows) && ps >= ld * cols;
+}
+
+// Q formation order: forward (Q += (Q W_k) Y_k^T after each panel, overlapping the
+// factorisation; 1.4x the md pairs of backward at M = K) for dd, where the panel
+// chain bounds the solve; backward for qd/od, which are GEMM bound.  MDLS_QFORM =
+// forward|backward overrides.
+template <int MM>
+inline bool q_forward() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MDLS_QFORM");
+    if (e && e[0] == 'f') v = 1;
+    else if (e && e[0] == 'b') v = 0;
+    else v = (MM == 2) ? 1 : 0;
+  }
+  return v == 1;
 }
 
 inline int tile_ok(int64_t Mr, int64_t K, int64_t nb) {
@@ -114,6 +132,9 @@ static QrBufs<M> qr_bufs(void* work, const Plan& p, int64_t Mr, int64_t K, int64
   b.X = Mat{at<double>(work, p.x), nb, nb * mx};
   b.part = at<double>(work, p.part);
   b.part_cap = kMaxSplit * nb * mx;
+  b.xbase = b.X.p;
+  b.pbase = b.part;
+  b.xcap = nb * mx;
   b.info_slot = at<int>(work, p.info);
   return b;
 }
@@ -139,8 +160,12 @@ int MDLS_FN(mdls_qr_)(int64_t Mr, int64_t K, int64_t nb, double* A, int64_t lda,
     cudaMemsetAsync(b.W.p, 0, sizeof(double) * M * Mr * K, st);
   }
   Mat Am{A, lda, psa};
-  if (qr_factor<M>(st, Mr, K, nb, Am, b, 0, K / nb, true) != cudaSuccess) return MDLS_ERR_CUDA;
-  if (Q) form_q_backward<M>(st, Mr, K, nb, Mat{Q, ldq, psq}, b);
+  Mat Qm{Q, ldq, psq};
+  const bool fwd = Q && q_forward<M>();
+  if (qr_factor_overlap<M>(b.lane(0, st), b.lane(1, side_stream(0)), b.lane(2, side_stream(1)), Mr, K, nb, Am, b,
+                           fwd ? &Qm : nullptr) != cudaSuccess)
+    return MDLS_ERR_CUDA;
+  if (Q && !fwd) form_q_backward<M>(st, Mr, K, nb, Qm, b);
   if (dev_info) MDLS_LAUNCH(F_MISC, st, info_finish_kernel<<<1, 1, 0, st>>>(b.info_slot, nullptr, dev_info));
   return launched();
 }
@@ -214,11 +239,14 @@ int MDLS_FN(mdls_lstsq_)(int64_t Mr, int64_t K, int64_t nb, const double* A, int
   MDLS_LAUNCH(F_MISC, st, copy_kernel<M><<<grid_for(Mr * K, 256), 256, 0, st>>>(Mr, K, CMat{A, lda, psa}, Af, 0));
   cudaMemsetAsync(bb.Y.p, 0, sizeof(double) * M * Mr * K, st);
   cudaMemsetAsync(bb.W.p, 0, sizeof(double) * M * Mr * K, st);
-  if (qr_factor<M>(st, Mr, K, nb, Af, bb, 0, K / nb, true) != cudaSuccess) return MDLS_ERR_CUDA;
+  Mat Q = (form_q && Q_out) ? Mat{Q_out, ldq, psq} : Mat{form_q ? at<double>(work, p.q) : nullptr, Mr, Mr * Mr};
+  const bool fwd = form_q && q_forward<M>();
+  if (qr_factor_overlap<M>(bb.lane(0, st), bb.lane(1, side_stream(0)), bb.lane(2, side_stream(1)), Mr, K, nb, Af, bb,
+                           fwd ? &Q : nullptr) != cudaSuccess)
+    return MDLS_ERR_CUDA;
   double* yv = at<double>(work, p.v1);
   if (form_q) {
-    Mat Q = Q_out ? Mat{Q_out, ldq, psq} : Mat{at<double>(work, p.q), Mr, Mr * Mr};
-    form_q_backward<M>(st, Mr, K, nb, Q, bb);
+    if (!fwd) form_q_backward<M>(st, Mr, K, nb, Q, bb);
     set_stage(MDLS_ST_QTB);
     gemm<M, true, false>(st, Mr, 1, Mr, cm(Q), CMat{b, Mr, psb}, Mat{yv, Mr, Mr}, 0, bb.part, bb.part_cap);
   } else {
@@ -257,7 +285,8 @@ int MDLS_FN(mdls_qr_panel_)(int64_t Mr, int64_t nb, int64_t k, double* Ak, int64
     cudaMemset2DAsync(Yk + l * psy, sizeof(double) * ldy, 0, sizeof(double) * Mr, nb, st);
   }
   // beta: per panel, stored in the workspace (indexed by global column)
-  if (qr_panel<M>(st, Mr, nb, k, Ag, Yg, Wg, b.beta - j0, nb, b) != cudaSuccess) return MDLS_ERR_CUDA;
+  const Lane L = b.lane(0, st);
+  if (qr_panel<M>(L, L, Mr, nb, k, Ag, Yg, Wg, b.beta - j0, nb, b) != cudaSuccess) return MDLS_ERR_CUDA;
   if (dev_info) MDLS_LAUNCH(F_MISC, st, info_finish_kernel<<<1, 1, 0, st>>>(b.info_slot, nullptr, dev_info));
   return launched();
 }
@@ -278,7 +307,8 @@ int MDLS_FN(mdls_qr_update_)(int64_t Mr, int64_t nb, int64_t k, const double* Wk
   set_stage(MDLS_NSTAGES);
   QrBufs<M> b = qr_bufs(work, p, std::max<int64_t>(Mr, c1), std::max<int64_t>(c1, nb), nb, nullptr, 0, 0);
   const int64_t j0 = k * nb;
-  qr_apply_panel<M>(st, Mr, nb, k, CMat{Yk + j0, ldy, psy}, CMat{Wk + j0, ldw, psw}, Mat{A, lda, psa}, c0, c1, b);
+  qr_apply_panel<M>(b.lane(0, st), Mr, nb, k, CMat{Yk + j0, ldy, psy}, CMat{Wk + j0, ldw, psw}, Mat{A, lda, psa}, c0,
+                    c1);
   return launched();
 }
 

@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(NT) leaf_kernel(LeafArgs<M> a) {
   constexpr int NRG = NT / TPR;   // row groups
   constexpr int GS = (NT / B >= 32) ? 32 : (NT / B >= 16 ? 16 : (NT / B >= 8 ? 8 : (NT / B >= 4 ? 4 : (NT / B >= 2 ? 2 : 1))));
   static_assert(V >= 1 && B % TPR == 0, "leaf shape");
-  static_assert(NT % B == 0 || B > NT, "leaf threads");
+  static_assert(NT % B == 0 && B * NW <= NT && 32 % NW == 0 && NW >= 4, "leaf threads");
 
   cg::cluster_group cluster = cg::this_cluster();
   const int C = (int)cluster.num_blocks();
@@ -126,7 +126,6 @@ __global__ void __launch_bounds__(NT) leaf_kernel(LeafArgs<M> a) {
   __shared__ md<M> SY[B][B];  // SY[p][l] = Y_p^T v_l (p < l)
   __shared__ md<M> Ts[B][B];  // leaf T, Ts[row][col]
   __shared__ md<M> sc_mu, sc_v1, sc_beta, sc_rv1;
-  __shared__ int sc_deg;
 
   auto T_ = [&](int64_t i, int c, int l) -> double& { return tile[((int64_t)l * B + c) * R + i]; };
 
@@ -179,16 +178,22 @@ __global__ void __launch_bounds__(NT) leaf_kernel(LeafArgs<M> a) {
       for (int q = 0; q < WE; ++q) wpart[warp][h * V + base + q] = acc[q];
     }
     __syncthreads();
-    if (tid < B) {
-      md<M> s = wpart[0][tid];
-      for (int w = 1; w < NW; ++w) s = add<M>(s, wpart[w][tid]);
-      red[buf][tid] = s;
-      if (rank == p_piv) {
-        md<M> pvv;
+    if (tid < ((B * NW + 31) / 32) * 32) {  // cross-warp sum, fixed shuffle tree (whole warps)
+      const int c = tid / NW, w = tid % NW;
+      md<M> s = (c < B) ? wpart[w][c] : md_zero<M>();
 #pragma unroll
-        for (int k = 0; k < M; ++k) pvv.v[k] = T_(pr, tid, k);
-        piv[buf][tid] = pvv;
+      for (int d = NW / 2; d >= 1; d >>= 1) {
+        md<M> o = shfl_down<M>(s, d);
+        if (w + d < NW) s = add<M>(s, o);
       }
+      if (w == 0 && c < B) red[buf][c] = s;
+    }
+    if (rank == p_piv && tid >= NT - B) {
+      const int c = tid - (NT - B);
+      md<M> pvv;
+#pragma unroll
+      for (int k = 0; k < M; ++k) pvv.v[k] = T_(pr, c, k);
+      piv[buf][c] = pvv;
     }
     LEAF_MARK(l, 2);
     cluster.sync();
@@ -197,14 +202,17 @@ __global__ void __launch_bounds__(NT) leaf_kernel(LeafArgs<M> a) {
     // (4) fixed-order sum of the C partials (DSMEM), pivot row from its owner
     if (tid < B * GS) {
       const int c = tid / GS, sub = tid % GS;
-      md<M> s = md_zero<M>();
-      bool have = false;
-      for (int q = sub; q < C; q += GS) {
-        const md<M>* rp = cluster.map_shared_rank(&red[buf][c], q);
-        md<M> t = *rp;
-        s = have ? add<M>(s, t) : t;
-        have = true;
+      constexpr int QPL = 16 / GS > 0 ? 16 / GS : 1;  // partials per lane (C <= 16)
+      md<M> t[QPL];
+#pragma unroll
+      for (int u = 0; u < QPL; ++u) {  // issue all DSMEM loads first
+        const int q = sub + u * GS;
+        t[u] = (q < C) ? *cluster.map_shared_rank(&red[buf][c], q) : md_zero<M>();
       }
+      md<M> s = t[0];
+#pragma unroll
+      for (int u = 1; u < QPL; ++u)
+        if (sub + u * GS < C) s = add<M>(s, t[u]);
 #pragma unroll
       for (int d = GS / 2; d >= 1; d >>= 1) {
         md<M> o = shfl_down<M>(s, d);
@@ -218,42 +226,56 @@ __global__ void __launch_bounds__(NT) leaf_kernel(LeafArgs<M> a) {
     __syncthreads();
     LEAF_MARK(l, 4);
 
-    // (5) Householder scalars (every CTA, identical); CTA 0 builds T column l-1 meanwhile
+    // (5) Householder scalars, every CTA identically (GVL Alg. 5.1.1, rewritten so
+    // the three divisions are independent): mu = sqrt(x1^2 + sigma);
+    //   x1 > 0:  s = x1 + mu, v1 = -sigma/s, 1/v1 = -s/sigma, beta = sigma/(mu s)
+    //   x1 <= 0: v1 = x1 - mu,               beta = -v1/mu
+    // (beta = 2 v1^2/(sigma + v1^2) in both cases, as sigma + v1^2 = -2 mu v1).
+    // Meanwhile this CTA's warp 1 extends its rows of the leaf T by column l-1.
+    const md<M> sigma = G[l], x1 = pv[l];
+    const bool deg = sigma.v[0] == 0.0;
+    const bool pos = x1.v[0] > 0.0;
     if (tid == 0) {
-      const md<M> sigma = G[l], x1 = pv[l];
-      if (sigma.v[0] == 0.0) {
-        sc_deg = 1;
-        sc_mu = x1;
-        sc_v1 = md_from<M>(1.0);
-      } else {
-        sc_deg = 0;
-        md<M> mu, v1;
-        house_v1<M>(sigma, x1, mu, v1);
-        sc_mu = mu;
-        sc_v1 = v1;
-      }
-    } else if (rank == 0 && warp == NW - 1 && l > 0) {
-      // T(:, l-1): T(ll, ll) = beta_ll; T(r, ll) = -beta_ll * sum_{p=r}^{ll-1} T(r, p) SY[p][ll]
-      const int ll = l - 1, r = lane;
-      if (r < ll) {
-        md<M> s = md_zero<M>();
-        for (int p = r; p < ll; ++p) s = fma<M>(s, Ts[r][p], SY[p][ll]);
-        Ts[r][ll] = neg(mul<M>(betas[ll], s));
-      } else if (r == ll) {
-        Ts[ll][ll] = betas[ll];
+      sc_mu = deg ? x1 : sqrt<M>(add<M>(mul<M>(x1, x1), sigma));
+    } else if (tid == 32 % NT && !deg && pos) {
+      sc_rv1 = md_recip<M>(sigma);  // 1/sigma for now
+    } else if (warp == 2 && l > 0) {
+      // T(r, ll) = -beta_ll sum_{p=r}^{ll-1} T(r, p) SY[p][ll] for the rows r = rank (mod C)
+      const int ll = l - 1;
+      for (int r = rank; r <= ll; r += C) {
+        if (r == ll) {
+          if (lane == 0) Ts[ll][ll] = betas[ll];
+          continue;
+        }
+        md<M> s = (lane >= r && lane < ll) ? mul<M>(Ts[r][lane], SY[lane][ll]) : md_zero<M>();
+        s = warp_sum<M>(s);
+        if (lane == 0) Ts[r][ll] = neg(mul<M>(betas[ll], s));
       }
     }
     __syncthreads();
     LEAF_MARK(l, 5);
-    if (tid == 0) {
-      sc_beta = sc_deg ? md_zero<M>() : house_beta<M>(G[l], sc_v1);
-    } else if (tid == 32 % NT) {
-      sc_rv1 = sc_deg ? md_from<M>(1.0) : md_recip<M>(sc_v1);
+    if (!deg) {
+      if (tid == 0) {
+        sc_beta = md_recip<M>(sc_mu);  // 1/mu for now
+      } else if (tid == 32 % NT) {
+        if (pos) sc_v1 = md_recip<M>(add<M>(x1, sc_mu));  // 1/s for now
+        else sc_rv1 = md_recip<M>(sub<M>(x1, sc_mu));
+      }
     }
     __syncthreads();
     LEAF_MARK(l, 6);
-    const md<M> beta = sc_beta, rv1 = sc_rv1;
-    const int deg = sc_deg;
+    md<M> beta, rv1;
+    if (deg) {
+      beta = md_zero<M>();
+      rv1 = md_from<M>(1.0);
+    } else if (pos) {
+      const md<M> s = add<M>(x1, sc_mu);
+      rv1 = neg(mul<M>(s, sc_rv1));              // -s / sigma
+      beta = mul<M>(mul<M>(sigma, sc_v1), sc_beta);  // sigma (1/s) (1/mu)
+    } else {
+      rv1 = sc_rv1;
+      beta = neg(mul<M>(sub<M>(x1, sc_mu), sc_beta));  // -v1 / mu
+    }
     // (6) w_c = beta (a_jc + rv1 g_c) for c > l; Y_c^T v = y_jc + rv1 g_c for c < l
     if (tid < B) {
       const int c = tid;
@@ -316,14 +338,16 @@ __global__ void __launch_bounds__(NT) leaf_kernel(LeafArgs<M> a) {
   }
 
   // ---- last T column, write-back of R/v, explicit Y, beta, T ----
-  if (rank == 0 && warp == NW - 1) {
-    const int ll = B - 1, r = lane;
-    if (r < ll) {
-      md<M> s = md_zero<M>();
-      for (int p = r; p < ll; ++p) s = fma<M>(s, Ts[r][p], SY[p][ll]);
-      Ts[r][ll] = neg(mul<M>(betas[ll], s));
-    } else if (r == ll) {
-      Ts[ll][ll] = betas[ll];
+  if (warp == 2) {
+    const int ll = B - 1;
+    for (int r = rank; r <= ll; r += C) {
+      if (r == ll) {
+        if (lane == 0) Ts[ll][ll] = betas[ll];
+        continue;
+      }
+      md<M> s = (lane >= r && lane < ll) ? mul<M>(Ts[r][lane], SY[lane][ll]) : md_zero<M>();
+      s = warp_sum<M>(s);
+      if (lane == 0) Ts[r][ll] = neg(mul<M>(betas[ll], s));
     }
   }
   for (int64_t e = tid; e < Rp * B; e += NT) {
@@ -338,12 +362,11 @@ __global__ void __launch_bounds__(NT) leaf_kernel(LeafArgs<M> a) {
     }
   }
   __syncthreads();
-  if (rank == 0) {
-    if (tid < B) st<M>(a.beta, a.bps, a.js + tid, betas[tid]);
-    for (int e = tid; e < B * B; e += NT) {
-      const int r = e % B, c = e / B;
-      st<M>(a.T.p, a.T.ps, r + (int64_t)c * a.T.ld, (r <= c) ? Ts[r][c] : md_zero<M>());
-    }
+  if (rank == 0 && tid < B) st<M>(a.beta, a.bps, a.js + tid, betas[tid]);
+  for (int e = tid; e < B * B; e += NT) {  // this CTA's rows of T (r = rank mod C), zeros below the diagonal
+    const int r = e % B, c = e / B;
+    if (r % C != rank) continue;
+    st<M>(a.T.p, a.T.ps, r + (int64_t)c * a.T.ld, (r <= c) ? Ts[r][c] : md_zero<M>());
   }
   cluster.sync();  // keep every CTA's shared memory alive until all DSMEM reads are done
 }
@@ -354,7 +377,7 @@ __global__ void __launch_bounds__(NT) leaf_kernel(LeafArgs<M> a) {
 // ---------------------------------------------------------------------------
 template <int M, int B, int TPR>
 cudaError_t leaf_launch_impl(cudaStream_t st, const LeafArgs<M>& la, int C) {
-  constexpr int NT = 128;
+  constexpr int NT = (64 * TPR < 128) ? 128 : 64 * TPR;  // >= 4 warps: warp 2 is free for T
   auto kern = leaf_kernel<M, B, TPR, NT>;
   const size_t smem = sizeof(double) * (size_t)M * (B + 1) * la.R;
   cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -398,12 +421,12 @@ cudaError_t launch_leaf(cudaStream_t st, int64_t Mrows, int64_t js, int64_t bmax
     switch (B) {
       case 16:
         if constexpr (M == 2) {
-          e = leaf_launch_impl<M, 16, 2>(st, la, C);
+          e = leaf_launch_impl<M, 16, 4>(st, la, C);
           break;
         }
         [[fallthrough]];
-      case 8: e = leaf_launch_impl<M, 8, 2>(st, la, C); break;
-      case 4: e = leaf_launch_impl<M, 4, 2>(st, la, C); break;
+      case 8: e = leaf_launch_impl<M, 8, 4>(st, la, C); break;
+      case 4: e = leaf_launch_impl<M, 4, 4>(st, la, C); break;
       case 2: e = leaf_launch_impl<M, 2, 2>(st, la, C); break;
       default: e = leaf_launch_impl<M, 1, 1>(st, la, C); break;
     }

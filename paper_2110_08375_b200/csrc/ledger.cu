@@ -51,6 +51,34 @@ cudaEvent_t get_event() {
 
 void set_stage(int stage) { t_stage = stage; }
 
+// two library-owned non-blocking side streams per device (joined into the
+// caller's stream by events in every call, so graph capture and ordering hold)
+cudaStream_t side_stream(int which) {
+  static std::mutex mu;
+  static std::vector<cudaStream_t> streams;  // [device * 2 + which]
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  const size_t idx = (size_t)dev * 2 + (which & 1);
+  if (streams.size() <= idx) streams.resize(idx + 1, nullptr);
+  if (!streams[idx]) cudaStreamCreateWithFlags(&streams[idx], cudaStreamNonBlocking);
+  return streams[idx];
+}
+
+// round-robin pool of timing-free events (an event may be re-recorded once the
+// waits on its previous record have been enqueued, which program order ensures)
+cudaEvent_t pool_event() {
+  static std::mutex mu;
+  static std::vector<cudaEvent_t> pool;
+  static size_t next = 0;
+  std::lock_guard<std::mutex> lk(mu);
+  if (pool.empty()) {
+    pool.resize(4096);
+    for (auto& e : pool) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  }
+  return pool[next++ % pool.size()];
+}
+
 void trace_begin(cudaStream_t st, int family) {
   (void)family;
   g_launches.fetch_add(1, std::memory_order_relaxed);

@@ -48,8 +48,8 @@ Plan make_plan(int op, int64_t Mr, int64_t K, int64_t nb) {
   }
   if (op == MDLS_OP_APPLY_QT) p.y = take(md * Mr * K);
   if (qr_like || op == MDLS_OP_APPLY_QT) {
-    p.x = take(md * nb * mx);
-    p.part = take(md * kMaxSplit * nb * mx);
+    p.x = take(3 * md * nb * mx);  // one GEMM-intermediate buffer per stream lane
+    p.part = take(3 * md * kMaxSplit * nb * mx);
   }
   p.v0 = take(md * mx);
   p.v1 = take(md * mx);
@@ -64,6 +64,14 @@ Plan make_plan(int op, int64_t Mr, int64_t K, int64_t nb) {
 // ---------------------------------------------------------------------------
 // Algorithm 2 on A (M x K), panels of width nb; fills Y (explicit), W, beta.
 // ---------------------------------------------------------------------------
+// per-stream GEMM scratch: intermediate X and split-K partials
+struct Lane {
+  cudaStream_t st;
+  Mat X;          // nb x max(M, K) (also used as an M x nb operand)
+  double* part;
+  int64_t cap;
+};
+
 template <int M>
 struct QrBufs {
   Mat Y, W;
@@ -72,6 +80,12 @@ struct QrBufs {
   double* part;
   int64_t part_cap;
   int* info_slot;
+  double* xbase;  // 3 lanes of X / part
+  double* pbase;
+  int64_t xcap;
+  Lane lane(int i, cudaStream_t st) const {
+    return Lane{st, Mat{xbase + (int64_t)i * xcap * M, X.ld, X.ps}, pbase + (int64_t)i * part_cap * M, part_cap};
+  }
 };
 
 // Panel k of Algorithm 2: factor columns [j0, j0+nb) in leaves of
@@ -81,61 +95,126 @@ struct QrBufs {
 //                                                 "update R" as two md GEMMs)
 //   W_s += W_<s (Y_<s^T W_s) (block form of z = -beta (v + W Y^T v))
 // so the panel's W (P_WY = I + W Y^T) is built column block by block.
+// The chain (leaf, W_s, in-panel update) runs on lane L0; the W-block
+// recurrence, which nothing in the chain waits for, on lane L2 (may be L0).
 template <int M>
-cudaError_t qr_panel(cudaStream_t st, int64_t Mr, int64_t nb, int64_t k, Mat A, Mat Y, Mat W, double* beta,
-                     int64_t bps, const QrBufs<M>& b) {
+cudaError_t qr_panel(const Lane& L0, const Lane& L2, int64_t Mr, int64_t nb, int64_t k, Mat A, Mat Y, Mat W,
+                     double* beta, int64_t bps, const QrBufs<M>& b) {
   const int64_t j0 = k * nb, r = Mr - j0;
   int64_t js = j0;
   while (js < j0 + nb) {
     int bw = 1;
     set_stage(MDLS_ST_PANEL);
     Mat Tl{b.T.p, 16, 256};
-    cudaError_t e = launch_leaf<M>(st, Mr, js, j0 + nb - js, A, Y, beta, bps, Tl, b.info_slot, &bw);
+    cudaError_t e = launch_leaf<M>(L0.st, Mr, js, j0 + nb - js, A, Y, beta, bps, Tl, b.info_slot, &bw);
     if (e != cudaSuccess) return e;
     const int64_t rs = Mr - js;
     const CMat Ys = sub(cm(Y), js, js);
     Mat Ws = sub(W, js, js);
     set_stage(MDLS_ST_WY);
-    gemm<M, false, false>(st, rs, bw, bw, Ys, cm(Tl), Ws, 3, nullptr, 0);  // W_s = -Y_s T_s
+    gemm<M, false, false>(L0.st, rs, bw, bw, Ys, cm(Tl), Ws, 3, nullptr, 0);  // W_s = -Y_s T_s
+    if (js > j0 && L2.st != L0.st) {
+      cudaEvent_t ev = pool_event();
+      cudaEventRecord(ev, L0.st);
+      cudaStreamWaitEvent(L2.st, ev, 0);
+    }
     const int64_t rem = j0 + nb - (js + bw);
     if (rem > 0) {
       set_stage(MDLS_ST_PANEL);
       Mat Cs = sub(A, js, js + bw);
-      gemm<M, true, false>(st, bw, rem, rs, cm(Ws), cm(Cs), b.X, 0, b.part, b.part_cap);
-      gemm<M, false, false>(st, rs, rem, bw, Ys, cm(b.X), Cs, 1, nullptr, 0);
+      gemm<M, true, false>(L0.st, bw, rem, rs, cm(Ws), cm(Cs), L0.X, 0, L0.part, L0.cap);
+      gemm<M, false, false>(L0.st, rs, rem, bw, Ys, cm(L0.X), Cs, 1, nullptr, 0);
     }
     if (js > j0) {
       set_stage(MDLS_ST_WY);
       const int64_t np = js - j0;
-      gemm<M, true, false>(st, np, bw, rs, sub(cm(Y), js, j0), cm(Ws), b.X, 0, b.part, b.part_cap);
-      gemm<M, false, false>(st, r, bw, np, sub(cm(W), j0, j0), cm(b.X), sub(W, j0, js), 1, nullptr, 0);
+      gemm<M, true, false>(L2.st, np, bw, rs, sub(cm(Y), js, j0), cm(Ws), L2.X, 0, L2.part, L2.cap);
+      gemm<M, false, false>(L2.st, r, bw, np, sub(cm(W), j0, j0), cm(L2.X), sub(W, j0, js), 1, nullptr, 0);
     }
     js += bw;
   }
-  (void)r;
   return cudaGetLastError();
 }
 
 // apply panel k to the columns [c0, c1) of A: C += Y_k (W_k^T C) ("YWT * C", "R + YWTC")
 template <int M>
-void qr_apply_panel(cudaStream_t st, int64_t Mr, int64_t nb, int64_t k, CMat Yk, CMat Wk, Mat A, int64_t c0,
-                    int64_t c1, const QrBufs<M>& b) {
+void qr_apply_panel(const Lane& L, int64_t Mr, int64_t nb, int64_t k, CMat Yk, CMat Wk, Mat A, int64_t c0,
+                    int64_t c1) {
   if (c1 <= c0) return;
   const int64_t j0 = k * nb, r = Mr - j0;
   set_stage(MDLS_ST_TRAILING);
   Mat Cm = sub(A, j0, c0);
-  gemm<M, true, false>(st, nb, c1 - c0, r, Wk, cm(Cm), b.X, 0, b.part, b.part_cap);
-  gemm<M, false, false>(st, r, c1 - c0, nb, Yk, cm(b.X), Cm, 1, nullptr, 0);
+  gemm<M, true, false>(L.st, nb, c1 - c0, r, Wk, cm(Cm), L.X, 0, L.part, L.cap);
+  gemm<M, false, false>(L.st, r, c1 - c0, nb, Yk, cm(L.X), Cm, 1, nullptr, 0);
+}
+
+// forward Q accumulation step (the paper's Q = Q + Q W Y^T):
+// Q(:, j0:) += (Q(:, j0:) W_k) Y_k^T
+template <int M>
+void form_q_forward_step(const Lane& L, int64_t Mr, int64_t nb, int64_t k, Mat Q, CMat Yk, CMat Wk) {
+  const int64_t j0 = k * nb, r = Mr - j0;
+  set_stage(MDLS_ST_FORM_Q);
+  Mat Xq{L.X.p, Mr, Mr * nb};
+  Mat Qs = sub(Q, 0, j0);
+  gemm<M, false, false>(L.st, Mr, nb, r, cm(Qs), Wk, Xq, 0, L.part, L.cap);        // "Q * WY^T"
+  gemm<M, false, true>(L.st, Mr, r, nb, cm(Xq), Yk, Qs, 1, nullptr, 0);            // "Q + QWY"
+}
+
+// Algorithm 2 with look-ahead over three streams: L0 carries the critical chain
+// (panel k+1 starts as soon as panel k is applied to its columns), L1 the rest
+// of the trailing update and the forward Q accumulation, L2 the W-block
+// recurrence.  Q (nullable) is formed forward on L1 when q_forward, else the
+// caller forms it backward afterwards.  All streams are joined into L0.
+template <int M>
+cudaError_t qr_factor_overlap(const Lane& L0, const Lane& L1, const Lane& L2, int64_t Mr, int64_t K, int64_t nb,
+                              Mat A, const QrBufs<M>& b, Mat* Qf) {
+  auto fork = [](cudaStream_t from, cudaStream_t to) {
+    if (from == to) return;
+    cudaEvent_t ev = pool_event();
+    cudaEventRecord(ev, from);
+    cudaStreamWaitEvent(to, ev, 0);
+  };
+  fork(L0.st, L1.st);
+  fork(L0.st, L2.st);
+  if (Qf) {
+    set_stage(MDLS_ST_FORM_Q);
+    MDLS_LAUNCH(F_MISC, L1.st, set_identity_kernel<M><<<grid_for(Mr * Mr, 256), 256, 0, L1.st>>>(Mr, Mr, *Qf));
+  }
+  const int64_t N = K / nb;
+  cudaEvent_t trail_done = nullptr;  // L1: trailing update of the previous panel finished
+  for (int64_t k = 0; k < N; ++k) {
+    const int64_t j0 = k * nb;
+    cudaError_t e = qr_panel<M>(L0, L2, Mr, nb, k, A, b.Y, b.W, b.beta, K, b);
+    if (e != cudaSuccess) return e;
+    fork(L0.st, L2.st);  // W_k complete on L2 after this point
+    cudaEvent_t wk = pool_event();
+    cudaEventRecord(wk, L2.st);
+    const CMat Yk = sub(cm(b.Y), j0, j0), Wk = sub(cm(b.W), j0, j0);
+    if (k + 1 < N) {
+      cudaStreamWaitEvent(L0.st, wk, 0);
+      if (trail_done) cudaStreamWaitEvent(L0.st, trail_done, 0);  // panel k+1's columns had panel k-1 applied
+      qr_apply_panel<M>(L0, Mr, nb, k, Yk, Wk, A, j0 + nb, j0 + 2 * nb);  // look-ahead
+    }
+    cudaStreamWaitEvent(L1.st, wk, 0);
+    qr_apply_panel<M>(L1, Mr, nb, k, Yk, Wk, A, j0 + 2 * nb, K);
+    trail_done = pool_event();
+    cudaEventRecord(trail_done, L1.st);
+    if (Qf) form_q_forward_step<M>(L1, Mr, nb, k, *Qf, Yk, Wk);
+  }
+  fork(L1.st, L0.st);
+  fork(L2.st, L0.st);
+  return cudaGetLastError();
 }
 
 template <int M>
 cudaError_t qr_factor(cudaStream_t st, int64_t Mr, int64_t K, int64_t nb, Mat A, const QrBufs<M>& b, int64_t kbeg,
                       int64_t kend, bool trailing) {
+  const Lane L = b.lane(0, st);
   for (int64_t k = kbeg; k < kend; ++k) {
     const int64_t j0 = k * nb;
-    cudaError_t e = qr_panel<M>(st, Mr, nb, k, A, b.Y, b.W, b.beta, K, b);
+    cudaError_t e = qr_panel<M>(L, L, Mr, nb, k, A, b.Y, b.W, b.beta, K, b);
     if (e != cudaSuccess) return e;
-    if (trailing) qr_apply_panel<M>(st, Mr, nb, k, sub(cm(b.Y), j0, j0), sub(cm(b.W), j0, j0), A, j0 + nb, K, b);
+    if (trailing) qr_apply_panel<M>(L, Mr, nb, k, sub(cm(b.Y), j0, j0), sub(cm(b.W), j0, j0), A, j0 + nb, K);
   }
   return cudaGetLastError();
 }
@@ -150,8 +229,9 @@ void form_q_backward(cudaStream_t st, int64_t Mr, int64_t K, int64_t nb, Mat Q, 
     const int64_t j0 = k * nb, r = Mr - j0;
     const CMat Yp = sub(cm(b.Y), j0, j0), Wp = sub(cm(b.W), j0, j0);
     Mat Qs = sub(Q, j0, j0);
-    gemm<M, true, false>(st, nb, r, r, Yp, cm(Qs), b.X, 0, b.part, b.part_cap);
-    gemm<M, false, false>(st, r, r, nb, Wp, cm(b.X), Qs, 1, nullptr, 0);
+    const Lane L = b.lane(0, st);
+    gemm<M, true, false>(st, nb, r, r, Yp, cm(Qs), L.X, 0, L.part, L.cap);
+    gemm<M, false, false>(st, r, r, nb, Wp, cm(L.X), Qs, 1, nullptr, 0);
   }
 }
 

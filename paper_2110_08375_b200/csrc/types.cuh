@@ -30,6 +30,9 @@ enum Family { F_GEMM = 0, F_PANEL = 1, F_INVERT = 2, F_BS = 3, F_MISC = 4, F_NFA
 void trace_begin(cudaStream_t st, int family);
 void trace_end(cudaStream_t st, int family);
 void set_stage(int stage);
+// side streams / event pool for the look-ahead QR (ledger.cu)
+cudaStream_t side_stream(int which);
+cudaEvent_t pool_event();
 #define MDLS_LAUNCH(FAM, ST, ...)          \
   do {                                     \
     ::mdls::trace_begin((ST), (FAM));      \

@@ -92,3 +92,46 @@ def to_mp(x: np.ndarray):
     m = x.shape[0]
     flat = x.reshape(m, -1)
     return [sum((Fraction(float(flat[k, i])) for k in range(m)), Fraction(0)) for i in range(flat.shape[1])]
+
+
+def lu_upper_torch(n: int, prec, seed: int, device="cuda"):
+    """Large-n variant of lu_upper generated on the device with torch (seeded
+    Philox/cuRAND stream + cuSOLVER LU, fp64): returns a CUDA tensor (m, n, n),
+    column-major planes, strict lower part exactly zero.  Lower limbs are
+    u * ulp(limb above) / 2 as in random_md (ulp via nextafter: exact)."""
+    import torch
+
+    m = limbs(prec)
+    g = torch.Generator(device=device)
+    g.manual_seed(int(seed))
+    a = torch.rand((n, n), generator=g, dtype=torch.float64, device=device) * 2.0 - 1.0
+    lu, _ = torch.linalg.lu_factor(a)
+    del a
+    u = torch.triu(lu)
+    del lu
+    out = torch.empty((m, n, n), dtype=torch.float64, device=device)
+    out[0] = u.T  # column-major plane: out[0, col, row] = U[row, col]
+    del u
+    mask = torch.triu(torch.ones((n, n), dtype=torch.bool, device=device)).T  # [col, row]: row <= col
+    for k in range(1, m):
+        prev = out[k - 1].abs()
+        ulp = torch.nextafter(prev, torch.full_like(prev, float("inf"))) - prev
+        r = torch.rand((n, n), generator=g, dtype=torch.float64, device=device) * 2.0 - 1.0
+        out[k] = torch.where(mask & (out[k - 1] != 0), r * ulp * 0.5, torch.zeros_like(r))
+        del prev, ulp, r
+    return out
+
+
+def random_vector_torch(n: int, prec, seed: int, device="cuda"):
+    import torch
+
+    m = limbs(prec)
+    g = torch.Generator(device=device)
+    g.manual_seed(int(seed) + 7919)
+    out = torch.empty((m, n), dtype=torch.float64, device=device)
+    out[0] = torch.rand(n, generator=g, dtype=torch.float64, device=device) * 2.0 - 1.0
+    for k in range(1, m):
+        prev = out[k - 1].abs()
+        ulp = torch.nextafter(prev, torch.full_like(prev, float("inf"))) - prev
+        out[k] = (torch.rand(n, generator=g, dtype=torch.float64, device=device) * 2.0 - 1.0) * ulp * 0.5
+    return out

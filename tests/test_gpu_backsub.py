@@ -74,3 +74,31 @@ def test_backsub_singular_reports_row(mdls, dev):
     x, info = mdls.backsub("dd", torch.from_numpy(U).to(dev), torch.from_numpy(y).to(dev), nb)
     torch.cuda.synchronize()
     assert int(info.item()) == 38
+
+
+def test_backsub_config4_full_sampled(orc, mdls, dev):
+    """BASELINE config 4 at full size: quad double, n = 17,920, tiles of 128 (the
+    bench's launch configuration).  U is generated on the device (LU of a seeded
+    uniform matrix).  Checked on sampled rows with the oracle: the
+    residual (U x - y)_i, md dot products accumulated by the oracle, within
+    1e3 * n * u * sum_c |U_ic x_c|."""
+    prec, n, nb = "qd", 17920, 128
+    U = inputs.lu_upper_torch(n, prec, seed=4, device=dev)
+    y = inputs.random_vector_torch(n, prec, seed=4, device=dev)
+    x, info = mdls.backsub(prec, U, y, nb)
+    torch.cuda.synchronize()
+    assert int(info.item()) == 0
+    xh = x.cpu().numpy()
+    yh = y.cpu().numpy()
+    assert np.all(np.isfinite(xh))
+    rng = np.random.default_rng(0)
+    rows = sorted(set([0, 1, nb - 1, nb, n - nb - 1, n - nb, n - 2, n - 1] + list(rng.integers(0, n, 40))))
+    u = U_OF[prec]
+    for i in rows:
+        urow = np.ascontiguousarray(U[:, i:, i].cpu().numpy())  # U(i, c), c >= i
+        xs = np.ascontiguousarray(xh[:, i:])
+        s = orc.dot(prec, urow, xs)
+        r = orc.md_op("sub", prec, s[:, None], yh[:, i:i + 1])[0, 0]
+        scale = float(np.sum(np.abs(urow[0] * xs[0])))
+        assert abs(r) <= 1e3 * n * u * scale, (i, r, scale)
+    del U

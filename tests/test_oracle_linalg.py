@@ -249,3 +249,14 @@ def test_lstsq_vs_exact_normal_equations(orc, prec, M, K, integer):
         got = sum((Fraction(float(x[k, i])) for k in range(m)), Fraction(0))
         assert abs(got - xe[i]) <= tol * xnorm, i
     assert orc.inv_normal(prec, A, x, b) <= 1e3 * M * U_OF[prec]
+
+
+@pytest.mark.parametrize("prec", PRECS)
+def test_dot_exact_rationals(orc, prec):
+    a = inputs.random_md((40,), prec, 21)
+    b = inputs.random_md((40,), prec, 22)
+    got = sum(Fraction(float(v)) for v in orc.dot(prec, a, b))
+    ea, eb = exact(a), exact(b)
+    ref = sum((ea[i] * eb[i] for i in range(40)), Fraction(0))
+    scale = sum((abs(ea[i] * eb[i]) for i in range(40)), Fraction(0))
+    assert abs(got - ref) <= Fraction(1000 * 40) * Fraction(U_OF[prec]) * scale
