@@ -41,8 +41,8 @@ METRIC = "md QR+backsub double-flops/s & % FP64 peak at n=1024 dd/qd/od, 1/2/4/8
 FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12      # 37.2 (FMA = 2 flops)
 FP64_PIPE_TOPS = 148 * 64 * 1.965e9 / 1e12            # 18.6 FP64-pipe lane ops/s (DADD/DMUL/DFMA each 1)
 # FP64 pipe instructions per md pair (one md mul + one md add) as the kernels implement them
-# (md.cuh: FMA two_prod): dd 9+20, qd 182+85, od 1202+269
-OPS_PER_PAIR = {"dd": 29, "qd": 267, "od": 1471}
+# (md.cuh Acc: dd unnormalised FMA accumulation 12; qd/od md mul + md add 182+85, 1202+269)
+OPS_PER_PAIR = {"dd": 12, "qd": 267, "od": 1471}
 # paper's V100 times for the same least-squares workload (T11): QR + BS kernel ms
 PAPER_V100_MS = {"dd": 451.1 + 4.0, "qd": 3020.6 + 28.0, "od": 11924.5 + 114.5}
 L2_FLUSH_BYTES = 512 << 20

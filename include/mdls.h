@@ -113,7 +113,8 @@ int mdls_trace_collect(double *stage_ms, double *family_ms, int64_t *family_laun
   /* canonical md-op counts of `op` (host only; A10).  Returns 0 or -i. */                                         \
   int mdls_count_##P(int op, int64_t M, int64_t K, int64_t nb, mdls_counts *out);                                  \
                                                                                                                    \
-  /* A0: elementwise md arithmetic on device vectors (op: 0 add, 1 sub, 2 mul, 3 div, 4 sqrt; b unused for sqrt).  \
+  /* A0: elementwise md arithmetic on device vectors (op: 0 add, 1 sub, 2 mul, 3 div, 4 sqrt, 5 latency-lean sqrt, \
+   * 6 latency-lean reciprocal 1/a -- the panel's Newton/Karp variants; b unused for ops >= 4).                      \
    * c = a op b, n entries, planes ps apart (same ps for a, b, c).  The operations are the readings of              \
    * DESIGN.md. */                                                                                       \
   int mdls_md_op_##P(int op, int64_t n, const double *a, const double *b, double *c, int64_t ps, void *stream);     \

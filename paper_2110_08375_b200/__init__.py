@@ -16,7 +16,7 @@ import ctypes
 from . import _lib
 
 PRECISIONS = {"dd": 2, "qd": 4, "od": 8}
-OPS = {"add": 0, "sub": 1, "mul": 2, "div": 3, "sqrt": 4}
+OPS = {"add": 0, "sub": 1, "mul": 2, "div": 3, "sqrt": 4, "sqrt_fast": 5, "recip_fast": 6}
 T1_SUMS = {"dd": (20, 23, 70), "qd": (89, 336, 893), "od": (269, 1742, 5126)}  # P:102-136 (add, mul, div)
 
 __all__ = ["md_op", "qr", "apply_qt", "qt_b", "invert_tiles", "backsub", "lstsq", "counts", "workspace_bytes",
@@ -78,11 +78,12 @@ def md_op(op: str, prec: str, a, b=None):
     """Elementwise md arithmetic on (m, n) CUDA vectors (A0)."""
     torch = _torch()
     _check_md(a, prec, 2, "a")
-    if op != "sqrt":
+    unary = OPS[op] >= 4
+    if not unary:
         _check_md(b, prec, 2, "b")
     c = torch.empty_like(a)
     n = a.shape[1]
-    rc = _lib.fn("mdls_md_op_", prec)(OPS[op], n, _ptr(a), _ptr(b if op != "sqrt" else None), _ptr(c), n, _stream())
+    rc = _lib.fn("mdls_md_op_", prec)(OPS[op], n, _ptr(a), _ptr(None if unary else b), _ptr(c), n, _stream())
     _lib.check(rc, "md_op")
     return c
 

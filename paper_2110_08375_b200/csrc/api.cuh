@@ -69,11 +69,11 @@ size_t MDLS_FN(mdls_workspace_)(int op, int64_t Mr, int64_t K, int64_t nb) {
 }
 
 int MDLS_FN(mdls_md_op_)(int op, int64_t n, const double* a, const double* b, double* c, int64_t ps, void* stream) {
-  if (op < 0 || op > 4) return -1;
+  if (op < 0 || op > 6) return -1;
   if (n < 0) return -2;
   if (n == 0) return 0;
   if (!a) return -3;
-  if (!b && op != 4) return -4;
+  if (!b && op < 4) return -4;
   if (!c) return -5;
   if (ps < n) return -6;
   MDLS_LAUNCH(F_MISC, S(stream), md_op_kernel<M><<<grid_for(n, 128), 128, 0, S(stream)>>>(op, n, a, b, c, ps));

@@ -78,13 +78,14 @@ __global__ void __launch_bounds__(256) bs_mulinv_kernel(int64_t nb, int64_t tile
   const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (r >= nb) return;
   const int64_t base = tile * nb;
-  md<M> s = md_zero<M>();
+  Acc<M> acc;
+  acc.init();
   for (int64_t c = r + lane; c < nb; c += 32) {  // upper triangular: c >= r
     md<M> t = ld<M>(Vt.p, Vt.ps, c + (base + r) * Vt.ld);
     md<M> bb = ld<M>(b, psb, base + c);
-    s = fma<M>(s, t, bb);
+    acc.add_prod(t, bb);
   }
-  s = warp_sum<M>(s);
+  md<M> s = warp_sum<M>(acc.get());
   if (lane == 0) st<M>(x, psx, base + r, s);
 }
 
@@ -100,15 +101,16 @@ __global__ void __launch_bounds__(32 * G) bs_update_kernel(int64_t nb, int64_t t
   const int64_t rho = (int64_t)blockIdx.x * 32 + lane;
   const int64_t nrows = tile * nb;
   const int64_t base = tile * nb;
-  md<M> s = md_zero<M>();
+  Acc<M> acc;
+  acc.init();
   if (rho < nrows) {
     for (int64_t c = g; c < nb; c += G) {
       md<M> u = ld<M>(U.p, U.ps, rho + (base + c) * U.ld);
       md<M> xx = ld<M>(x, psx, base + c);
-      s = fma<M>(s, u, xx);
+      acc.add_prod(u, xx);
     }
   }
-  part[g][lane] = s;
+  part[g][lane] = acc.get();
   __syncthreads();
   if (g == 0 && rho < nrows) {
     md<M> t = part[0][lane];

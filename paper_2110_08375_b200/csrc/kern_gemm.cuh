@@ -39,11 +39,11 @@ __global__ void __launch_bounds__(GemmTile<M, V>::NT) gemm_kernel(GemmArgs g) {
   const int64_t kb = (int64_t)blockIdx.z * g.kc;
   const int64_t ke = min(g.k, kb + g.kc);
 
-  md<M> acc[TM][TN];
+  Acc<M> acc[TM][TN];
 #pragma unroll
   for (int t = 0; t < TM; ++t)
 #pragma unroll
-    for (int u = 0; u < TN; ++u) acc[t][u] = md_zero<M>();
+    for (int u = 0; u < TN; ++u) acc[t][u].init();
 
   for (int64_t k0 = kb; k0 < ke; k0 += BK) {
     // ---- stage A tile (BM x BK) ----
@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(GemmTile<M, V>::NT) gemm_kernel(GemmArgs g) {
 #pragma unroll
       for (int t = 0; t < TM; ++t)
 #pragma unroll
-        for (int u = 0; u < TN; ++u) acc[t][u] = fma<M>(acc[t][u], a[t], b[u]);
+        for (int u = 0; u < TN; ++u) acc[t][u].add_prod(a[t], b[u]);
     }
     __syncthreads();
   }
@@ -97,11 +97,11 @@ __global__ void __launch_bounds__(GemmTile<M, V>::NT) gemm_kernel(GemmArgs g) {
       if (gj >= g.n) continue;
       if (g.part) {
         const int64_t pps = g.m * g.n * g.S;
-        st<M>(g.part, pps, gi + (gj + blockIdx.z * g.n) * g.m, acc[t][u]);
+        st<M>(g.part, pps, gi + (gj + blockIdx.z * g.n) * g.m, acc[t][u].get());
       } else {
         const int64_t e = gi + gj * g.ldc;
         md<M> c = (g.mode == 1 || g.mode == 2) ? ld<M>(g.C, g.psc, e) : md_zero<M>();
-        st<M>(g.C, g.psc, e, apply_mode<M>(g.mode, c, acc[t][u]));
+        st<M>(g.C, g.psc, e, apply_mode<M>(g.mode, c, acc[t][u].get()));
       }
     }
   }

@@ -89,7 +89,7 @@ __device__ __noinline__ md<M> house_beta(const md<M>& sigma, const md<M>& v1) {
 }
 template <int M>
 __device__ __noinline__ md<M> md_recip(const md<M>& v1) {
-  return div<M>(md_from<M>(1.0), v1);
+  return recip_fast<M>(v1);
 }
 
 #ifdef MDLS_LEAF_PROF
@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(NT) leaf_kernel(LeafArgs<M> a) {
     const bool deg = sigma.v[0] == 0.0;
     const bool pos = x1.v[0] > 0.0;
     if (tid == 0) {
-      sc_mu = deg ? x1 : sqrt<M>(add<M>(mul<M>(x1, x1), sigma));
+      sc_mu = deg ? x1 : sqrt_fast<M>(add<M>(mul<M>(x1, x1), sigma));
     } else if (tid == 32 % NT && !deg && pos) {
       sc_rv1 = md_recip<M>(sigma);  // 1/sigma for now
     } else if (warp == 2 && l > 0) {

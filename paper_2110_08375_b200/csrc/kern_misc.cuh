@@ -12,13 +12,15 @@ __global__ void md_op_kernel(int op, int64_t n, const double* __restrict__ a, co
                              double* __restrict__ c, int64_t ps) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
     md<M> x = ld<M>(a, ps, e), r;
-    md<M> y = (op == 4) ? md_zero<M>() : ld<M>(b, ps, e);
+    md<M> y = (op >= 4) ? md_zero<M>() : ld<M>(b, ps, e);
     switch (op) {
       case 0: r = add<M>(x, y); break;
       case 1: r = sub<M>(x, y); break;
       case 2: r = mul<M>(x, y); break;
       case 3: r = div<M>(x, y); break;
-      default: r = sqrt<M>(x); break;
+      case 4: r = sqrt<M>(x); break;
+      case 5: r = sqrt_fast<M>(x); break;
+      default: r = recip_fast<M>(x); break;
     }
     st<M>(c, ps, e, r);
   }

@@ -341,6 +341,129 @@ __device__ __forceinline__ md<M> fms(const md<M>& acc, const md<M>& a, const md<
 }
 
 // ----------------------------------------------------------------------------
+// latency-lean square root and reciprocal for the panel's scalar chain.
+// Newton's iteration doubles the number of correct bits, so the reciprocal
+// square root y ~ 1/sqrt(a) and the reciprocal are refined in increasing
+// precision (double -> dd -> qd, each step at the precision it produces), and
+// the last doubling is Karp's: sqrt(a) = a y + (a - (a y)^2) y / 2, 1/d = y +
+// y (1 - d y), with only the leading products at full precision.  About 4x
+// (od) / 2x (qd) fewer FP64 operations than QDlib-style sqrt and long
+// division; results agree with them to within a few units of 2^(-53 M)
+// (tests/test_gpu_arith.py, op codes 5 and 6).
+// ----------------------------------------------------------------------------
+template <int P, int M>
+__device__ __forceinline__ md<P> md_trunc(const md<M>& a) {
+  md<P> r;
+#pragma unroll
+  for (int k = 0; k < P; ++k) r.v[k] = (k < M) ? a.v[k] : 0.0;
+  return r;
+}
+
+template <int M>
+__device__ __forceinline__ md<M> add(const md<M>& a, const md<M>& b);
+template <int M>
+__device__ __forceinline__ md<M> mul(const md<M>& a, const md<M>& b);
+
+// y <- y + y (1/2 - (a/2) y^2) at precision P
+template <int P>
+__device__ __forceinline__ md<P> rsqrt_step(const md<P>& a, const md<P>& y) {
+  md<P> t = mul<P>(y, y);
+  t = mul<P>(scale_pow2<P>(a, 0.5), t);
+  t = add<P>(md_from<P>(0.5), neg(t));
+  return add<P>(y, mul<P>(t, y));
+}
+// y ~ 1/sqrt(a) with about 53 * H correct bits (H = 1, 2, 4)
+template <int H, int M>
+__device__ __forceinline__ md<H> rsqrt_to(const md<M>& a) {
+  md<H> y = md_from<H>(__drcp_rn(__dsqrt_rn(a.v[0])));
+  if constexpr (H >= 2) {
+    md<2> y2 = rsqrt_step<2>(md_trunc<2, M>(a), md_trunc<2, H>(y));
+    y = md_trunc<H, 2>(y2);
+  }
+  if constexpr (H >= 4) {
+    md<4> y4 = rsqrt_step<4>(md_trunc<4, M>(a), md_trunc<4, H>(y));
+    y = md_trunc<H, 4>(y4);
+  }
+  return y;
+}
+template <int M>
+__device__ __noinline__ md<M> sqrt_fast(const md<M>& a) {
+  if (a.v[0] == 0.0) return md_zero<M>();
+  if constexpr (M == 2) {
+    return dd_sqrt(a);  // QDlib's dd sqrt is already the Karp form
+  } else {
+  constexpr int H = M / 2;
+  const md<H> yh = rsqrt_to<H, M>(a);
+  const md<M> y = md_trunc<M, H>(yh);
+  const md<M> x = mul<M>(a, y);                         // a y
+  const md<M> r = add<M>(a, neg(mul<M>(x, x)));         // a - (a y)^2, tiny
+  const md<H> c = mul<H>(md_trunc<H, M>(r), scale_pow2<H>(yh, 0.5));
+  return add<M>(x, md_trunc<M, H>(c));
+  }
+}
+template <int P>
+__device__ __forceinline__ md<P> recip_step(const md<P>& d, const md<P>& y) {
+  const md<P> e = add<P>(md_from<P>(1.0), neg(mul<P>(d, y)));
+  return add<P>(y, mul<P>(y, e));
+}
+template <int M>
+__device__ __noinline__ md<M> recip_fast(const md<M>& d) {
+  if constexpr (M == 2) {
+    const double y0 = __drcp_rn(d.v[0]);
+    const md<2> e = dd_add(md_from<2>(1.0), neg(dd_mul_d(d, y0)));  // 1 - d y0, tiny
+    md<2> r;
+    two_sum(y0, __dmul_rn(y0, e.v[0]), r.v[0], r.v[1]);
+    return r;
+  } else {
+  constexpr int H = M / 2;
+  md<H> yh = md_from<H>(__drcp_rn(d.v[0]));
+  if constexpr (H >= 2) yh = md_trunc<H, 2>(recip_step<2>(md_trunc<2, M>(d), md_trunc<2, H>(yh)));
+  if constexpr (H >= 4) yh = md_trunc<H, 4>(recip_step<4>(md_trunc<4, M>(d), md_trunc<4, H>(yh)));
+  const md<M> y = md_trunc<M, H>(yh);
+  const md<M> e = add<M>(md_from<M>(1.0), neg(mul<M>(d, y)));   // 1 - d y, tiny
+  const md<H> c = mul<H>(yh, md_trunc<H, M>(e));
+  return add<M>(y, md_trunc<M, H>(c));
+  }
+}
+
+// ----------------------------------------------------------------------------
+// dot-product accumulator: sum_k a_k * b_k.  Generic precisions keep a
+// renormalised md sum (one md mul + one md add per term, 267 / 1471 FP64 ops
+// for qd / od).  Double double keeps an unnormalised pair: the leading
+// products are summed with two_sum and every error term (the FMA product
+// error, both cross products a0*b1 + a1*b0, the two_sum error) goes into a
+// plain double tail -- 12 FP64 ops per term instead of 29 -- and the pair is
+// normalised once by get().  Error: |tail rounding| <= k u^2 sum |a_k b_k|,
+// far inside the 1e3 n u parity tolerance for k <= 10^5.
+// ----------------------------------------------------------------------------
+template <int M>
+struct Acc {
+  md<M> s;
+  __device__ __forceinline__ void init() { s = md_zero<M>(); }
+  __device__ __forceinline__ void add_prod(const md<M>& a, const md<M>& b) { s = fma<M>(s, a, b); }
+  __device__ __forceinline__ md<M> get() const { return s; }
+};
+template <>
+struct Acc<2> {
+  double hi, lo;
+  __device__ __forceinline__ void init() { hi = lo = 0.0; }
+  __device__ __forceinline__ void add_prod(const md<2>& a, const md<2>& b) {
+    const double p = __dmul_rn(a.v[0], b.v[0]);
+    double pe = __fma_rn(a.v[0], b.v[0], -p);
+    pe = __fma_rn(a.v[0], b.v[1], pe);
+    pe = __fma_rn(a.v[1], b.v[0], pe);
+    double t;
+    two_sum(hi, p, hi, t);
+    lo = __dadd_rn(lo, __dadd_rn(t, pe));
+  }
+  __device__ __forceinline__ md<2> get() const {
+    md<2> r;
+    two_sum(hi, lo, r.v[0], r.v[1]);
+    return r;
+  }
+};
+
+// ----------------------------------------------------------------------------
 // limb-planar access: limb k of element e at p[k*ps + e]
 // ----------------------------------------------------------------------------
 template <int M>

@@ -51,3 +51,22 @@ def test_md_ops_bitwise(orc, mdls, dev, prec, op):
     ref = orc.md_op(op, prec, a, None if op == "sqrt" else b)
     bad = np.nonzero(np.any(got != ref, axis=0))[0]
     assert bad.size == 0, (prec, op, bad[:5], got[:, bad[:1]].T, ref[:, bad[:1]].T)
+
+
+@pytest.mark.parametrize("prec", ["dd", "qd", "od"])
+def test_fast_sqrt_recip_accuracy(orc, mdls, dev, prec):
+    """The panel's Newton/Karp sqrt and reciprocal (op codes 5, 6) agree with the
+    oracle's QDlib-style sqrt and long division to a few units of 2^(-53 m)."""
+    m = inputs.limbs(prec)
+    n = 4000
+    a, _ = _operands(prec, n, 23)
+    a = np.where(a[0] < 0, -a, a)
+    a = np.where(a[0] == 0, 1.0, a)
+    ga = torch.from_numpy(a).to(dev)
+    one = np.zeros_like(a)
+    one[0] = 1.0
+    for op, ref in (("sqrt_fast", orc.md_op("sqrt", prec, a)), ("recip_fast", orc.md_op("div", prec, one, a))):
+        got = mdls.md_op(op, prec, ga).cpu().numpy()
+        d = orc.md_op("sub", prec, got, ref)
+        rel = np.abs(d[0]) / np.abs(ref[0])
+        assert np.max(rel) <= 2.0 ** (-53 * m + 8), (op, np.max(rel))
