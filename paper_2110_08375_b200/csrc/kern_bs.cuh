@@ -90,37 +90,42 @@ __global__ void __launch_bounds__(256) bs_mulinv_kernel(int64_t nb, int64_t tile
 }
 
 // ============================================================================
-// A9: b(rho) -= sum_c U(rho, tile*nb + c) x_tile(c) for rho < tile*nb.
-// CTA = 32 rows x G column groups; fixed-order smem reduction over groups.
+// A9: b(rho) -= sum_c U(rho, tile*nb + c) x_tile(c) for rho in [row0, row1).
+// CTA = 32*RPT rows x G column groups: each thread keeps RPT independent row
+// accumulators over the columns c = g, g+G, ... (coalesced column reads of U),
+// then a fixed-order smem reduction over the G groups.
 // ============================================================================
-template <int M, int G>
-__global__ void __launch_bounds__(32 * G) bs_update_kernel(int64_t nb, int64_t tile, CMat U, const double* x,
-                                                           int64_t psx, double* b, int64_t psb) {
-  __shared__ md<M> part[G][32];
+template <int M, int G, int RPT>
+__global__ void __launch_bounds__(32 * G) bs_update_kernel(int64_t nb, int64_t tile, int64_t row0, int64_t row1, CMat U,
+                                                           const double* x, int64_t psx, double* b, int64_t psb) {
+  __shared__ md<M> part[G][32 * RPT];
   const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
-  const int64_t rho = (int64_t)blockIdx.x * 32 + lane;
-  const int64_t nrows = tile * nb;
+  const int64_t rbase = row0 + (int64_t)blockIdx.x * 32 * RPT;
   const int64_t base = tile * nb;
-  Acc<M> acc;
-  acc.init();
-  if (rho < nrows) {
-    for (int64_t c = g; c < nb; c += G) {
-      md<M> u = ld<M>(U.p, U.ps, rho + (base + c) * U.ld);
-      md<M> xx = ld<M>(x, psx, base + c);
-      acc.add_prod(u, xx);
+  Acc<M> acc[RPT];
+#pragma unroll
+  for (int t = 0; t < RPT; ++t) acc[t].init();
+  for (int64_t c = g; c < nb; c += G) {
+    const md<M> xx = ld<M>(x, psx, base + c);
+#pragma unroll
+    for (int t = 0; t < RPT; ++t) {
+      const int64_t rho = rbase + lane + 32 * t;
+      if (rho < row1) acc[t].add_prod(ld<M>(U.p, U.ps, rho + (base + c) * U.ld), xx);
     }
   }
-  part[g][lane] = acc.get();
-  __syncthreads();
-  if (g == 0 && rho < nrows) {
-    md<M> t = part[0][lane];
 #pragma unroll
-    for (int q = 1; q < G; ++q) t = add<M>(t, part[q][lane]);
+  for (int t = 0; t < RPT; ++t) part[g][lane + 32 * t] = acc[t].get();
+  __syncthreads();
+  for (int e = threadIdx.x; e < 32 * RPT; e += 32 * G) {
+    const int64_t rho = rbase + e;
+    if (rho >= row1) continue;
+    md<M> t = part[0][e];
+#pragma unroll
+    for (int q = 1; q < G; ++q) t = add<M>(t, part[q][e]);
     md<M> bb = ld<M>(b, psb, rho);
     st<M>(b, psb, rho, add<M>(bb, neg(t)));
   }
 }
-
 
 template <int M>
 void launch_invert(cudaStream_t st, int64_t ntiles, int64_t nb, CMat U, Mat Vt, double diag_scale, const double* dbeta,
@@ -141,18 +146,26 @@ void launch_bs_mulinv(cudaStream_t st, int64_t nb, int64_t tile, CMat Vt, const 
   MDLS_LAUNCH(F_BS, st, bs_mulinv_kernel<M><<<(unsigned)cdiv(nb, 8), 256, 0, st>>>(nb, tile, Vt, b, psb, x, psx));
 }
 
+// rows [row0, row1): few rows (the look-ahead tile) -> 32 column groups of one row
+// each; many rows (the bulk) -> 8 groups of two rows per thread
 template <int M>
-void launch_bs_update(cudaStream_t st, int64_t nb, int64_t tile, CMat U, const double* x, int64_t psx, double* b,
-                      int64_t psb) {
-  constexpr int G = 8;
-  MDLS_LAUNCH(F_BS, st, bs_update_kernel<M, G><<<(unsigned)cdiv(tile * nb, 32), 32 * G, 0, st>>>(nb, tile, U, x, psx, b, psb));
+void launch_bs_update(cudaStream_t st, int64_t nb, int64_t tile, int64_t row0, int64_t row1, CMat U, const double* x,
+                      int64_t psx, double* b, int64_t psb) {
+  const int64_t rows = row1 - row0;
+  if (rows <= 0) return;
+  constexpr int GC = (M == 2) ? 32 : 16;  // column groups for the look-ahead tile (registers / smem bound)
+  if (rows <= 512) {
+    MDLS_LAUNCH(F_BS, st, bs_update_kernel<M, GC, 1><<<(unsigned)cdiv(rows, 32), 32 * GC, 0, st>>>(nb, tile, row0, row1, U, x, psx, b, psb));
+  } else {
+    MDLS_LAUNCH(F_BS, st, bs_update_kernel<M, 8, 2><<<(unsigned)cdiv(rows, 64), 32 * 8, 0, st>>>(nb, tile, row0, row1, U, x, psx, b, psb));
+  }
 }
 
 #define MDLS_INSTANTIATE_BS(MM)                                                                                \
   template void launch_invert<MM>(cudaStream_t, int64_t, int64_t, CMat, Mat, double, const double*, int*);                    \
   template void launch_bs_mulinv<MM>(cudaStream_t, int64_t, int64_t, CMat, const double*, int64_t, double*,    \
                                      int64_t);                                                                 \
-  template void launch_bs_update<MM>(cudaStream_t, int64_t, int64_t, CMat, const double*, int64_t, double*,    \
-                                     int64_t);
+  template void launch_bs_update<MM>(cudaStream_t, int64_t, int64_t, int64_t, int64_t, CMat, const double*,  \
+                                     int64_t, double*, int64_t);
 
 }  // namespace mdls

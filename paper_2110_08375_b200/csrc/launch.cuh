@@ -23,7 +23,7 @@ void launch_bs_mulinv(cudaStream_t st, int64_t nb, int64_t tile, CMat Vt, const 
                       int64_t psx);
 
 template <int M>
-void launch_bs_update(cudaStream_t st, int64_t nb, int64_t tile, CMat U, const double* x, int64_t psx, double* b,
-                      int64_t psb);
+void launch_bs_update(cudaStream_t st, int64_t nb, int64_t tile, int64_t row0, int64_t row1, CMat U, const double* x,
+                      int64_t psx, double* b, int64_t psb);
 
 }  // namespace mdls

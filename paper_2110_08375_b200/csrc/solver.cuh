@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstring>
+#include <vector>
 
 #include "../../include/mdls.h"
 #include "launch.cuh"
@@ -250,21 +251,55 @@ void apply_qt_panels(cudaStream_t st, int64_t Mr, int64_t K, int64_t nb, CMat Y,
   }
 }
 
-// Algorithm 1: U x = y (leading n x n of U), tiles of nb
+// Algorithm 1: U x = y (leading n x n of U), N = n/nb tiles.
+// Tile inverses are computed in chunks, top tiles first, on a side stream; the
+// chain i = N..1 runs on `st`: x_i = U_i^-1 b_i, then the look-ahead update of
+// b_{i-1} only, while the bulk update b_j -= A_ji x_i (j < i-1) runs on a
+// second side stream (the paper's "simultaneously update") one step
+// behind.  Every b_j still receives its updates in the order i = N..j+1.
 template <int M>
 void backsub(cudaStream_t st, int64_t n, int64_t nb, CMat U, const double* y, int64_t psy, double* x, int64_t psx,
              Mat Vt, double* bwork, int* info_slot) {
   const int64_t N = n / nb;
+  cudaStream_t sinv = side_stream(1), sbulk = side_stream(0);
+  auto fork = [](cudaStream_t from, cudaStream_t to) {
+    cudaEvent_t ev = pool_event();
+    cudaEventRecord(ev, from);
+    cudaStreamWaitEvent(to, ev, 0);
+    return ev;
+  };
+  fork(st, sinv);
+  fork(st, sbulk);
+  // tile inverses, top chunk first
   set_stage(MDLS_ST_INVERT);
-  launch_invert<M>(st, N, nb, U, Vt, 1.0, nullptr, info_slot);
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(N, 16));
+  std::vector<cudaEvent_t> inv_ready((size_t)N, nullptr);
+  for (int64_t hi = N; hi > 0; hi -= chunk) {
+    const int64_t lo = std::max<int64_t>(0, hi - chunk);
+    launch_invert<M>(sinv, hi - lo, nb, sub(U, lo * nb, lo * nb), sub(Vt, 0, lo * nb), 1.0, nullptr, info_slot);
+    cudaEvent_t ev = pool_event();
+    cudaEventRecord(ev, sinv);
+    for (int64_t t = lo; t < hi; ++t) inv_ready[(size_t)t] = ev;
+  }
   // bwork = y (n entries)
   MDLS_LAUNCH(F_MISC, st, copy_kernel<M><<<grid_for(n, 256), 256, 0, st>>>(n, 1, CMat{y, n, psy}, Mat{bwork, n, n}, 0));
+  std::vector<cudaEvent_t> bulk_done((size_t)N + 2, nullptr);
   for (int64_t i = N - 1; i >= 0; --i) {
+    cudaStreamWaitEvent(st, inv_ready[(size_t)i], 0);
+    if (bulk_done[(size_t)i + 2]) cudaStreamWaitEvent(st, bulk_done[(size_t)i + 2], 0);
     set_stage(MDLS_ST_MULINV);
     launch_bs_mulinv<M>(st, nb, i, cm(Vt), bwork, n, x, psx);
     set_stage(MDLS_ST_BSUPDATE);
-    if (i > 0) launch_bs_update<M>(st, nb, i, U, x, psx, bwork, n);
+    if (i >= 1) launch_bs_update<M>(st, nb, i, (i - 1) * nb, i * nb, U, x, psx, bwork, n);
+    if (i >= 2) {
+      fork(st, sbulk);
+      launch_bs_update<M>(sbulk, nb, i, 0, (i - 1) * nb, U, x, psx, bwork, n);
+      bulk_done[(size_t)i] = pool_event();
+      cudaEventRecord(bulk_done[(size_t)i], sbulk);
+    }
   }
+  fork(sinv, st);
+  fork(sbulk, st);
 }
 
 }  // namespace mdls
