@@ -266,7 +266,8 @@ def qr_update(prec: str, Wk, Yk, A, k: int, nb: int, c0: int, c1: int, work=None
     if c1 <= c0:
         return
     if work is None:
-        work, nbytes = _work(prec, _lib.OP_QR, max(M, c1), max(c1, nb), nb, A.device)
+        Kw = -(-max(c1, nb) // nb) * nb
+        work, nbytes = _work(prec, _lib.OP_QR, max(M, Kw), Kw, nb, A.device)
     else:
         nbytes = work.numel()
     rc = _lib.fn("mdls_qr_update_", prec)(M, nb, k, *_mat(Wk), *_mat(Yk), *_mat(A), c0, c1, _ptr(work), nbytes,

@@ -146,19 +146,15 @@ void launch_bs_mulinv(cudaStream_t st, int64_t nb, int64_t tile, CMat Vt, const 
   MDLS_LAUNCH(F_BS, st, bs_mulinv_kernel<M><<<(unsigned)cdiv(nb, 8), 256, 0, st>>>(nb, tile, Vt, b, psb, x, psx));
 }
 
-// rows [row0, row1): few rows (the look-ahead tile) -> 32 column groups of one row
-// each; many rows (the bulk) -> 8 groups of two rows per thread
+// rows [row0, row1): CTA = 32 rows x GC column groups (1024 / 512 threads), so
+// even the short late steps spread over many SMs
 template <int M>
 void launch_bs_update(cudaStream_t st, int64_t nb, int64_t tile, int64_t row0, int64_t row1, CMat U, const double* x,
                       int64_t psx, double* b, int64_t psb) {
   const int64_t rows = row1 - row0;
   if (rows <= 0) return;
-  constexpr int GC = (M == 2) ? 32 : 16;  // column groups for the look-ahead tile (registers / smem bound)
-  if (rows <= 512) {
-    MDLS_LAUNCH(F_BS, st, bs_update_kernel<M, GC, 1><<<(unsigned)cdiv(rows, 32), 32 * GC, 0, st>>>(nb, tile, row0, row1, U, x, psx, b, psb));
-  } else {
-    MDLS_LAUNCH(F_BS, st, bs_update_kernel<M, 8, 2><<<(unsigned)cdiv(rows, 64), 32 * 8, 0, st>>>(nb, tile, row0, row1, U, x, psx, b, psb));
-  }
+  constexpr int GC = (M == 2) ? 32 : 16;  // column groups (registers / smem bound)
+  MDLS_LAUNCH(F_BS, st, bs_update_kernel<M, GC, 1><<<(unsigned)cdiv(rows, 32), 32 * GC, 0, st>>>(nb, tile, row0, row1, U, x, psx, b, psb));
 }
 
 #define MDLS_INSTANTIATE_BS(MM)                                                                                \

@@ -410,7 +410,7 @@ cudaError_t launch_leaf(cudaStream_t st, int64_t Mrows, int64_t js, int64_t bmax
   const int64_t rows = Mrows - js;
   const size_t cap = 200 * 1024;
   int B = 1;
-  while (B * 2 <= bmax && B * 2 <= (M == 2 ? 16 : 8)) B *= 2;
+  while (B * 2 <= bmax && B * 2 <= (M == 2 ? 16 : 8)) B *= 2;  // B = 32 measured slower per column
   for (;;) {
     const int C = (int)std::max<int64_t>(1, std::min<int64_t>(csize, rows));
     const int64_t R = cdiv(rows, C);
@@ -419,6 +419,12 @@ cudaError_t launch_leaf(cudaStream_t st, int64_t Mrows, int64_t js, int64_t bmax
     LeafArgs<M> la{Mrows, js, R, A, Y, beta, bps, T, info};
     cudaError_t e;
     switch (B) {
+      case 32:
+        if constexpr (M == 2) {
+          e = leaf_launch_impl<M, 32, 4>(st, la, C);
+          break;
+        }
+        [[fallthrough]];
       case 16:
         if constexpr (M == 2) {
           e = leaf_launch_impl<M, 16, 4>(st, la, C);

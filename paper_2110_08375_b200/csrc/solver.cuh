@@ -45,7 +45,7 @@ Plan make_plan(int op, int64_t Mr, int64_t K, int64_t nb) {
     p.w = take(md * Mr * K);
     p.beta = take(md * K);
     p.s = take(md * nb * nb);
-    p.t = take(md * std::max<int64_t>(nb * nb, 256));
+    p.t = take(md * std::max<int64_t>(nb * nb, 1024));
   }
   if (op == MDLS_OP_APPLY_QT) p.y = take(md * Mr * K);
   if (qr_like || op == MDLS_OP_APPLY_QT) {
@@ -106,7 +106,7 @@ cudaError_t qr_panel(const Lane& L0, const Lane& L2, int64_t Mr, int64_t nb, int
   while (js < j0 + nb) {
     int bw = 1;
     set_stage(MDLS_ST_PANEL);
-    Mat Tl{b.T.p, 16, 256};
+    Mat Tl{b.T.p, 32, 1024};  // leaf T, B <= 32
     cudaError_t e = launch_leaf<M>(L0.st, Mr, js, j0 + nb - js, A, Y, beta, bps, Tl, b.info_slot, &bw);
     if (e != cudaSuccess) return e;
     const int64_t rs = Mr - js;
@@ -252,25 +252,21 @@ void apply_qt_panels(cudaStream_t st, int64_t Mr, int64_t K, int64_t nb, CMat Y,
 }
 
 // Algorithm 1: U x = y (leading n x n of U), N = n/nb tiles.
-// Tile inverses are computed in chunks, top tiles first, on a side stream; the
-// chain i = N..1 runs on `st`: x_i = U_i^-1 b_i, then the look-ahead update of
-// b_{i-1} only, while the bulk update b_j -= A_ji x_i (j < i-1) runs on a
-// second side stream (the paper's "simultaneously update") one step
-// behind.  Every b_j still receives its updates in the order i = N..j+1.
+// Tile inverses are computed in chunks of 16 tiles, top first, on a side stream
+// so that the chain can start as soon as the last tiles are inverted; the chain
+// i = N..1 runs on `st`: x_i = U_i^-1 b_i, then b_j -= A_ji x_i for all j < i
+// in one launch (the paper's "simultaneously update").
 template <int M>
 void backsub(cudaStream_t st, int64_t n, int64_t nb, CMat U, const double* y, int64_t psy, double* x, int64_t psx,
              Mat Vt, double* bwork, int* info_slot) {
   const int64_t N = n / nb;
-  cudaStream_t sinv = side_stream(1), sbulk = side_stream(0);
+  cudaStream_t sinv = side_stream(1);
   auto fork = [](cudaStream_t from, cudaStream_t to) {
     cudaEvent_t ev = pool_event();
     cudaEventRecord(ev, from);
     cudaStreamWaitEvent(to, ev, 0);
-    return ev;
   };
   fork(st, sinv);
-  fork(st, sbulk);
-  // tile inverses, top chunk first
   set_stage(MDLS_ST_INVERT);
   const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(N, 16));
   std::vector<cudaEvent_t> inv_ready((size_t)N, nullptr);
@@ -283,23 +279,18 @@ void backsub(cudaStream_t st, int64_t n, int64_t nb, CMat U, const double* y, in
   }
   // bwork = y (n entries)
   MDLS_LAUNCH(F_MISC, st, copy_kernel<M><<<grid_for(n, 256), 256, 0, st>>>(n, 1, CMat{y, n, psy}, Mat{bwork, n, n}, 0));
-  std::vector<cudaEvent_t> bulk_done((size_t)N + 2, nullptr);
+  cudaEvent_t waited = nullptr;
   for (int64_t i = N - 1; i >= 0; --i) {
-    cudaStreamWaitEvent(st, inv_ready[(size_t)i], 0);
-    if (bulk_done[(size_t)i + 2]) cudaStreamWaitEvent(st, bulk_done[(size_t)i + 2], 0);
+    if (inv_ready[(size_t)i] != waited) {
+      cudaStreamWaitEvent(st, inv_ready[(size_t)i], 0);
+      waited = inv_ready[(size_t)i];
+    }
     set_stage(MDLS_ST_MULINV);
     launch_bs_mulinv<M>(st, nb, i, cm(Vt), bwork, n, x, psx);
     set_stage(MDLS_ST_BSUPDATE);
-    if (i >= 1) launch_bs_update<M>(st, nb, i, (i - 1) * nb, i * nb, U, x, psx, bwork, n);
-    if (i >= 2) {
-      fork(st, sbulk);
-      launch_bs_update<M>(sbulk, nb, i, 0, (i - 1) * nb, U, x, psx, bwork, n);
-      bulk_done[(size_t)i] = pool_event();
-      cudaEventRecord(bulk_done[(size_t)i], sbulk);
-    }
+    if (i >= 1) launch_bs_update<M>(st, nb, i, 0, i * nb, U, x, psx, bwork, n);
   }
   fork(sinv, st);
-  fork(sbulk, st);
 }
 
 }  // namespace mdls

@@ -58,9 +58,12 @@ class GpuOps(Ops):
         self.mdls.qr_update(prec, Wk, Yk, A, k, nb, c0, c1)
 
     def identity_cols(self, prec, Q, cols):
+        import torch
+
         Q.zero_()
-        for j, c in enumerate(cols):
-            Q[0, j, c] = 1.0
+        if len(cols):
+            idx = torch.arange(len(cols), device=Q.device)
+            Q[0, idx, torch.tensor(cols, device=Q.device)] = 1.0
 
     def qt_b_cols(self, prec, Q, b):
         return self.mdls.qt_b(prec, Q, b)

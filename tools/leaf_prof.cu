@@ -24,7 +24,7 @@ void run(int Mrows, int bmax) {
   cudaMalloc(&A, h.size() * 8);
   cudaMalloc(&Y, h.size() * 8);
   cudaMalloc(&beta, M * K * 8);
-  cudaMalloc(&T, M * 256 * 8);
+  cudaMalloc(&T, M * 1024 * 8);
   cudaMalloc(&info, 4);
   for (int rep = 0; rep < 3; ++rep) {
     cudaMemcpy(A, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
@@ -34,7 +34,7 @@ void run(int Mrows, int bmax) {
     cudaEventCreate(&e1);
     cudaEventRecord(e0);
     cudaError_t e = launch_leaf<M>(0, Mrows, 0, bmax, Mat{A, Mrows, (int64_t)Mrows * K}, Mat{Y, Mrows, (int64_t)Mrows * K},
-                                   beta, K, Mat{T, 16, 256}, info, &bw);
+                                   beta, K, Mat{T, 32, 1024}, info, &bw);
     cudaEventRecord(e1);
     cudaDeviceSynchronize();
     float ms;
