@@ -83,6 +83,10 @@ __global__ void __launch_bounds__(GemmTile<M, V>::NT) gemm_kernel(GemmArgs g) {
 #pragma unroll
         for (int u = 0; u < TN; ++u) acc[t][u].add_prod(a[t], b[u]);
     }
+#pragma unroll
+    for (int t = 0; t < TM; ++t)
+#pragma unroll
+      for (int u = 0; u < TN; ++u) acc[t][u].renorm_bins();
     __syncthreads();
   }
 

@@ -371,10 +371,320 @@ __global__ void __launch_bounds__(NT) leaf_kernel(LeafArgs<M> a) {
   cluster.sync();  // keep every CTA's shared memory alive until all DSMEM reads are done
 }
 
+// ===========================================================================
+// Register-resident leaf (rows per CTA <= NT/TPR): the same column step as
+// leaf_kernel with the latency taken out of the chain.
+//  * each thread keeps its row's V = B/TPR tile entries in registers; the TPR
+//    threads of a row are adjacent lanes, so the current column x_i reaches
+//    them by a shuffle and the update needs no block barrier;
+//  * products and every reduction level use the unnormalised accumulators of
+//    md.cuh (Acc: dd pair / qd-od level bins) -- exact merges, one
+//    normalisation per column sum;
+//  * the CTA partials are PUSHED into every CTA's shared memory (DSMEM stores,
+//    double buffered) together with the pivot row before the cluster barrier,
+//    so after it each CTA sums 16 local partials (no remote-load latency);
+//  * Householder scalars split over three threads: mu = sqrt(x1^2 + sigma)
+//    then 1/(x1 +- mu); 1/sigma; 1/mu = rsqrt(x1^2 + sigma) -- all
+//    independent after the reduction except the first chain.
+// Three __syncthreads and one cluster barrier per column.
+// ===========================================================================
+template <int M>
+__device__ __forceinline__ md<M> rsqrt_md(const md<M>& a) {
+  if constexpr (M == 8) {
+    const md<8> y = md_trunc<8, 4>(rsqrt_to<4, 8>(a));
+    return rsqrt_step<8>(a, y);
+  } else {
+    return rsqrt_to<M, M>(a);
+  }
+}
+
+template <int M, int V, int MASK, int TPR>
+struct HalveAcc {
+  // reduce-scatter of V accumulators over the lane bits >= TPR (see HalveSum)
+  __device__ __forceinline__ static void run(Acc<M>* v, int lane, int& base, int& plain) {
+    if constexpr (MASK >= TPR && MASK > 0) {
+      if constexpr (V > 1) {
+        constexpr int half = V / 2;
+        const bool up = (lane & MASK) != 0;
+#pragma unroll
+        for (int q = 0; q < half; ++q) {
+          Acc<M> send, keep;
+#pragma unroll
+          for (int k = 0; k < Acc<M>::NV; ++k) {
+            send.r(k) = up ? v[q].r(k) : v[q + half].r(k);
+            keep.r(k) = up ? v[q + half].r(k) : v[q].r(k);
+          }
+          keep.merge(acc_shfl_xor<M>(send, MASK));
+          v[q] = keep;
+        }
+        if (up) base += half;
+        HalveAcc<M, half, MASK / 2, TPR>::run(v, lane, base, plain);
+      } else {
+        v[0].merge(acc_shfl_xor<M>(v[0], MASK));
+        plain |= MASK;
+        HalveAcc<M, 1, MASK / 2, TPR>::run(v, lane, base, plain);
+      }
+    }
+  }
+  static constexpr int V_END = (MASK < TPR) ? V : HalveAcc<M, (V > 1 ? V / 2 : 1), MASK / 2, TPR>::V_END;
+};
+template <int M, int V, int TPR>
+struct HalveAcc<M, V, 0, TPR> {
+  __device__ __forceinline__ static void run(Acc<M>*, int, int&, int&) {}
+  static constexpr int V_END = V;
+};
+
+template <int M, int B, int TPR, int NT>
+__global__ void __launch_bounds__(NT) leaf_reg_kernel(LeafArgs<M> a) {
+  constexpr int V = B / TPR;
+  constexpr int NW = NT / 32;
+  constexpr int CMAX = 16;
+  constexpr int GS = 16;  // lanes per column in the final partial sum
+  static_assert(V >= 1 && B % TPR == 0 && 32 % TPR == 0, "leaf shape");
+  static_assert(B * NW <= NT && 32 % NW == 0 && NW >= 4 && B * GS <= NT, "leaf threads");
+
+  cg::cluster_group cluster = cg::this_cluster();
+  const int C = (int)cluster.num_blocks();
+  const int rank = (int)cluster.block_rank();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int h = tid % TPR, rg = tid / TPR;
+
+  __shared__ Acc<M> red[2][CMAX][B];  // pushed CTA partials [buffer][source rank][column]
+  __shared__ md<M> piv[2][B];         // pushed pivot row
+  __shared__ md<M> pvl[B];            // pivot row staging in the owner CTA
+  __shared__ Acc<M> wpart[NW][B];
+  __shared__ md<M> G[B], betas[B];
+  __shared__ md<M> SY[B][B];  // SY[p][l] = Y_p^T v_l (p < l)
+  __shared__ md<M> Ts[B][B];
+  __shared__ md<M> sc_mu, sc_rs, sc_rsig, sc_rmu;
+
+  const int64_t total = a.Mrows - a.js;
+  const int64_t row0 = a.js + (int64_t)rank * a.R;
+  int64_t Rp = total - (int64_t)rank * a.R;
+  Rp = Rp < 0 ? 0 : (Rp > a.R ? a.R : Rp);
+  const bool valid = rg < Rp;
+  const int64_t gi = row0 + rg;
+
+  md<M> t[V];
+#pragma unroll
+  for (int q = 0; q < V; ++q) {
+    const int c = h * V + q;
+#pragma unroll
+    for (int k = 0; k < M; ++k) t[q].v[k] = valid ? a.A.p[k * a.A.ps + (a.js + c) * a.A.ld + gi] : 0.0;
+  }
+
+  for (int l = 0; l < B; ++l) {
+    const int64_t j = a.js + l;
+    const int buf = l & 1;
+    const int p_piv = (int)((j - a.js) / a.R);
+    const int hl = l / V, ql = l % V;
+
+    LEAF_MARK(l, 0);
+    // (1) x_i from the row's owner lane of column l; products over the own row
+    md<M> x;
+#pragma unroll
+    for (int k = 0; k < M; ++k) x.v[k] = __shfl_sync(0xffffffffu, t[ql].v[k], (lane & ~(TPR - 1)) + hl);
+    const bool below = valid && gi > j;
+    Acc<M> acc[V];
+#pragma unroll
+    for (int q = 0; q < V; ++q) {
+      acc[q].init();
+      if (below) acc[q].add_prod(x, t[q]);
+    }
+    if (valid && gi == j) {
+#pragma unroll
+      for (int q = 0; q < V; ++q) pvl[h * V + q] = t[q];
+    }
+    LEAF_MARK(l, 1);
+    // (2) warp reduce-scatter, cross-warp sum, push to every CTA
+    int base = 0, plain = 0;
+    HalveAcc<M, V, 16, TPR>::run(acc, lane, base, plain);
+    constexpr int VE = HalveAcc<M, V, 16, TPR>::V_END;
+    if ((lane & plain) == 0) {
+#pragma unroll
+      for (int q = 0; q < VE; ++q) wpart[warp][h * V + base + q] = acc[q];
+    }
+    __syncthreads();
+    if (tid < B * NW) {
+      const int c = tid / NW, w = tid % NW;
+      Acc<M> s = wpart[w][c];
+#pragma unroll
+      for (int d = NW / 2; d >= 1; d >>= 1) {
+        Acc<M> o = acc_shfl_down<M>(s, d);
+        if (w + d < NW) s.merge(o);
+      }
+      // broadcast the CTA sum to the NW lanes of this column, which push it
+#pragma unroll
+      for (int k = 0; k < Acc<M>::NV; ++k) s.r(k) = __shfl_sync(0xffffffffu, s.r(k), (lane & ~(NW - 1)));
+      for (int q = w; q < C; q += NW) *cluster.map_shared_rank(&red[buf][rank][c], q) = s;
+    }
+    if (rank == p_piv) {
+      for (int e = tid; e < B * C; e += NT) {
+        const int c = e % B, q = e / B;
+        *cluster.map_shared_rank(&piv[buf][c], q) = pvl[c];
+      }
+    }
+    LEAF_MARK(l, 2);
+    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    LEAF_MARK(l, 3);
+
+    // (3) fixed-order sum of the C partials (local smem), GS lanes per column
+    if (tid < B * GS) {
+      const int c = tid / GS, q = tid % GS;
+      Acc<M> s;
+      if (q < C) s = red[buf][q][c];
+      else s.init();
+#pragma unroll
+      for (int d = GS / 2; d >= 1; d >>= 1) {
+        Acc<M> o = acc_shfl_down<M>(s, d);
+        if (q + d < GS) s.merge(o);
+      }
+      if (q == 0) G[c] = s.get();
+    }
+    __syncthreads();
+    LEAF_MARK(l, 4);
+
+    // (4) Householder scalars (GVL Alg. 5.1.1 with independent reciprocals):
+    //   x1 > 0:  s = x1 + mu, 1/v1 = -s/sigma, beta = sigma/(mu s)
+    //   x1 <= 0: v1 = x1 - mu, beta = -v1/mu
+    const md<M> sigma = G[l], x1 = piv[buf][l];
+    const bool deg = sigma.v[0] == 0.0;
+    const bool pos = x1.v[0] > 0.0;
+    if (!deg) {
+      if (tid == 0) {
+        const md<M> mu = sqrt_fast<M>(add<M>(mul<M>(x1, x1), sigma));
+        sc_mu = mu;
+        sc_rs = recip_fast<M>(pos ? add<M>(x1, mu) : sub<M>(x1, mu));
+      } else if (tid == 32) {
+        if (pos) sc_rsig = recip_fast<M>(sigma);
+      } else if (tid == 64) {
+        sc_rmu = rsqrt_md<M>(add<M>(mul<M>(x1, x1), sigma));
+      }
+    } else if (tid == 0) {
+      sc_mu = x1;
+    }
+    if (warp == 3 && l > 0) {  // extend this CTA's rows of the leaf T by column l-1
+      const int ll = l - 1;
+      for (int r = rank; r <= ll; r += C) {
+        if (r == ll) {
+          if (lane == 0) Ts[ll][ll] = betas[ll];
+          continue;
+        }
+        md<M> s = (lane >= r && lane < ll) ? mul<M>(Ts[r][lane], SY[lane][ll]) : md_zero<M>();
+        s = warp_sum<M>(s);
+        if (lane == 0) Ts[r][ll] = neg(mul<M>(betas[ll], s));
+      }
+    }
+    __syncthreads();
+    LEAF_MARK(l, 5);
+    const md<M> mu = sc_mu;
+    md<M> beta, rv1;
+    if (deg) {
+      beta = md_zero<M>();
+      rv1 = md_from<M>(1.0);
+    } else if (pos) {
+      rv1 = neg(mul<M>(add<M>(x1, mu), sc_rsig));
+      beta = mul<M>(mul<M>(sigma, sc_rs), sc_rmu);
+    } else {
+      rv1 = sc_rs;
+      beta = neg(mul<M>(sub<M>(x1, mu), sc_rmu));
+    }
+    if (tid < B) {
+      const int c = tid;
+      if (c < l) SY[c][l] = deg ? piv[buf][c] : add<M>(piv[buf][c], mul<M>(rv1, G[c]));
+      else if (c == l) betas[l] = beta;
+    }
+    LEAF_MARK(l, 6);
+    LEAF_MARK(l, 7);
+    // (5) update the own row: t_c -= v_i w_c (c > l), w_c = beta (a_jc + rv1 g_c); column l <- v
+    if (valid && gi >= j) {
+      const bool piv_row = gi == j;
+      const md<M> v = piv_row ? md_from<M>(1.0) : (deg ? x : mul<M>(x, rv1));
+#pragma unroll
+      for (int q = 0; q < V; ++q) {
+        const int c = h * V + q;
+        if (c > l && !deg) {
+          const md<M> w = mul<M>(beta, add<M>(piv[buf][c], mul<M>(rv1, G[c])));
+          t[q] = piv_row ? sub<M>(t[q], w) : fms<M>(t[q], v, w);
+        } else if (c == l) {
+          t[q] = piv_row ? mu : v;
+        }
+      }
+    }
+    if (tid == 0 && rank == 0) {
+      const double m0 = mu.v[0];
+      if (!(m0 != 0.0) || !isfinite(m0)) atomicMin(a.info, (int)(j + 1));
+    }
+    LEAF_MARK(l, 8);
+  }
+
+  // ---- last T column, write-back of R/v, explicit Y, beta, T ----
+  __syncthreads();
+  if (warp == 3) {
+    const int ll = B - 1;
+    for (int r = rank; r <= ll; r += C) {
+      if (r == ll) {
+        if (lane == 0) Ts[ll][ll] = betas[ll];
+        continue;
+      }
+      md<M> s = (lane >= r && lane < ll) ? mul<M>(Ts[r][lane], SY[lane][ll]) : md_zero<M>();
+      s = warp_sum<M>(s);
+      if (lane == 0) Ts[r][ll] = neg(mul<M>(betas[ll], s));
+    }
+  }
+  if (valid) {
+#pragma unroll
+    for (int q = 0; q < V; ++q) {
+      const int64_t jc = a.js + h * V + q;
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+        a.A.p[k * a.A.ps + jc * a.A.ld + gi] = t[q].v[k];
+        a.Y.p[k * a.Y.ps + jc * a.Y.ld + gi] = (gi < jc) ? 0.0 : (gi == jc ? (k == 0 ? 1.0 : 0.0) : t[q].v[k]);
+      }
+    }
+  }
+  __syncthreads();
+  if (rank == 0 && tid < B) st<M>(a.beta, a.bps, a.js + tid, betas[tid]);
+  for (int e = tid; e < B * B; e += NT) {
+    const int r = e % B, c = e / B;
+    if (r % C != rank) continue;
+    st<M>(a.T.p, a.T.ps, r + (int64_t)c * a.T.ld, (r <= c) ? Ts[r][c] : md_zero<M>());
+  }
+  cluster.sync();  // keep every CTA's shared memory alive until all DSMEM traffic is done
+}
+
+template <int M, int B, int TPR, int NT>
+cudaError_t leaf_reg_launch(cudaStream_t st, const LeafArgs<M>& la, int C) {
+  auto kern = leaf_reg_kernel<M, B, TPR, NT>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C, 1, 1);
+  cfg.blockDim = dim3(NT, 1, 1);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  trace_begin(st, F_PANEL);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, la);
+  trace_end(st, F_PANEL);
+  return e;
+}
+
 // ---------------------------------------------------------------------------
 // launcher: cluster size C (16, non-portable; 8 fallback), leaf width B
 // (power of two dividing nb, capped per precision and by shared memory)
 // ---------------------------------------------------------------------------
+// The shared-memory leaf is compiled in its own translation unit per precision
+// (leafsm_<p>.cu, MDLS_LEAF_SMEM_TU) to keep the od build parallel.
+template <int M, int B, int TPR>
+cudaError_t leaf_launch_impl(cudaStream_t st, const LeafArgs<M>& la, int C);
+#if defined(MDLS_LEAF_SMEM_TU)
 template <int M, int B, int TPR>
 cudaError_t leaf_launch_impl(cudaStream_t st, const LeafArgs<M>& la, int C) {
   constexpr int NT = (64 * TPR < 128) ? 128 : 64 * TPR;  // >= 4 warps: warp 2 is free for T
@@ -399,6 +709,15 @@ cudaError_t leaf_launch_impl(cudaStream_t st, const LeafArgs<M>& la, int C) {
   trace_end(st, F_PANEL);
   return e;
 }
+#endif
+#define MDLS_INSTANTIATE_LEAF_SMEM_WIDE(MM)                                             \
+  template cudaError_t leaf_launch_impl<MM, 32, 4>(cudaStream_t, const LeafArgs<MM>&, int); \
+  template cudaError_t leaf_launch_impl<MM, 16, 4>(cudaStream_t, const LeafArgs<MM>&, int);
+#define MDLS_INSTANTIATE_LEAF_SMEM(MM)                                                  \
+  template cudaError_t leaf_launch_impl<MM, 8, 4>(cudaStream_t, const LeafArgs<MM>&, int);  \
+  template cudaError_t leaf_launch_impl<MM, 4, 4>(cudaStream_t, const LeafArgs<MM>&, int);  \
+  template cudaError_t leaf_launch_impl<MM, 2, 2>(cudaStream_t, const LeafArgs<MM>&, int);  \
+  template cudaError_t leaf_launch_impl<MM, 1, 1>(cudaStream_t, const LeafArgs<MM>&, int);
 
 inline size_t leaf_smem_bytes(int M, int B, int64_t R) { return sizeof(double) * (size_t)M * (B + 1) * R; }
 
@@ -418,6 +737,21 @@ cudaError_t launch_leaf(cudaStream_t st, int64_t Mrows, int64_t js, int64_t bmax
     if (leaf_smem_bytes(M, B, R) > cap) return cudaErrorInvalidValue;
     LeafArgs<M> la{Mrows, js, R, A, Y, beta, bps, T, info};
     cudaError_t e;
+    static const bool force_smem = [] {
+      const char* v = getenv("MDLS_LEAF");
+      return v && v[0] == 's';
+    }();
+    if (!force_smem && B >= 4 && R <= 64) {
+      if constexpr (M == 2) e = (B == 16) ? leaf_reg_launch<M, 16, 4, 256>(st, la, C)
+                                          : (B == 8 ? leaf_reg_launch<M, 8, 4, 256>(st, la, C)
+                                                    : leaf_reg_launch<M, 4, 4, 256>(st, la, C));
+      else e = (B == 8) ? leaf_reg_launch<M, 8, 4, 256>(st, la, C) : leaf_reg_launch<M, 4, 4, 256>(st, la, C);
+    } else if (!force_smem && M <= 4 && B >= 4 && R <= 128) {
+      if constexpr (M == 2) e = (B == 16) ? leaf_reg_launch<M, 16, 4, 512>(st, la, C)
+                                          : (B == 8 ? leaf_reg_launch<M, 8, 4, 512>(st, la, C)
+                                                    : leaf_reg_launch<M, 4, 4, 512>(st, la, C));
+      else e = (B == 8) ? leaf_reg_launch<M, 8, 4, 512>(st, la, C) : leaf_reg_launch<M, 4, 4, 512>(st, la, C);
+    } else {
     switch (B) {
       case 32:
         if constexpr (M == 2) {
@@ -435,6 +769,7 @@ cudaError_t launch_leaf(cudaStream_t st, int64_t Mrows, int64_t js, int64_t bmax
       case 4: e = leaf_launch_impl<M, 4, 4>(st, la, C); break;
       case 2: e = leaf_launch_impl<M, 2, 2>(st, la, C); break;
       default: e = leaf_launch_impl<M, 1, 1>(st, la, C); break;
+    }
     }
     if (e == cudaSuccess || csize == 8) {
       *bw = B;

@@ -1,0 +1,6 @@
+// shared-memory leaf (rows per CTA beyond the register leaf) for od (8 limbs).
+#define MDLS_LEAF_SMEM_TU
+#include "kern_leaf.cuh"
+namespace mdls {
+MDLS_INSTANTIATE_LEAF_SMEM(8)
+}  // namespace mdls

@@ -436,12 +436,73 @@ __device__ __noinline__ md<M> recip_fast(const md<M>& d) {
 // normalised once by get().  Error: |tail rounding| <= k u^2 sum |a_k b_k|,
 // far inside the 1e3 n u parity tolerance for k <= 10^5.
 // ----------------------------------------------------------------------------
+//
+// Quad and octo double use the same idea with M "level bins" s[0..M-1]: the
+// limb products a_i b_j of level n = i + j <= M-2 are exact two_prods whose
+// high part is deposited into bin n and error into bin n+1; a deposit into
+// bin L is exact (two_sum, the error carried to bin L+1, ...) down to bin M-2,
+// and bin M-1 (levels M-1 and M, the same products baileyMul_fast keeps)
+// takes plain FMAs.  Only bin M-1 ever rounds, at magnitude ~u^(M-1) of the
+// terms, so the sum is accurate to a few units of u^M per term -- the same
+// order as one renormalised md mul + md add per term -- at about 112 (qd) /
+// 950 (od) FP64 operations per term instead of 267 / 1471.  renorm_bins()
+// (a bottom-up two_sum sweep) keeps the lower bins small; callers run it every
+// few terms (each k-tile), get() runs it and renormalises to an md number.
 template <int M>
 struct Acc {
-  md<M> s;
-  __device__ __forceinline__ void init() { s = md_zero<M>(); }
-  __device__ __forceinline__ void add_prod(const md<M>& a, const md<M>& b) { s = fma<M>(s, a, b); }
-  __device__ __forceinline__ md<M> get() const { return s; }
+  double s[M];
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int k = 0; k < M; ++k) s[k] = 0.0;
+  }
+  // exact deposit of t into bin L (two_sum cascade to bin M-2, plain add into bin M-1)
+  __device__ __forceinline__ void dep(int L, double t) {
+#pragma unroll
+    for (int j = 0; j < M - 1; ++j)
+      if (j >= L) two_sum(s[j], t, s[j], t);
+    s[M - 1] = __dadd_rn(s[M - 1], t);
+  }
+  __device__ __forceinline__ void add_prod(const md<M>& a, const md<M>& b) {
+    double tail = s[M - 1];
+#pragma unroll
+    for (int i = 0; i < M; ++i) tail = __fma_rn(a.v[i], b.v[M - 1 - i], tail);  // level M-1
+#pragma unroll
+    for (int i = 1; i < M; ++i) tail = __fma_rn(a.v[i], b.v[M - i], tail);      // level M
+    s[M - 1] = tail;
+#pragma unroll
+    for (int n = 0; n <= M - 2; ++n) {
+#pragma unroll
+      for (int i = 0; i <= n; ++i) {
+        double p, e;
+        two_prod(a.v[i], b.v[n - i], p, e);
+        dep(n, p);
+        dep(n + 1, e);
+      }
+    }
+  }
+  __device__ __forceinline__ void renorm_bins() {
+#pragma unroll
+    for (int j = M - 1; j >= 1; --j) two_sum(s[j - 1], s[j], s[j - 1], s[j]);
+  }
+  // exact merge of another accumulator (bin by bin)
+  __device__ __forceinline__ void merge(const Acc& o) {
+#pragma unroll
+    for (int L = 0; L < M; ++L) dep(L, o.s[L]);
+  }
+  static constexpr int NV = M;
+  __device__ __forceinline__ double& r(int i) { return s[i]; }
+  __device__ __forceinline__ double r(int i) const { return s[i]; }
+  __device__ __forceinline__ md<M> get() const {
+    double f[M + 1];
+#pragma unroll
+    for (int k = 0; k < M; ++k) f[k] = s[k];
+    f[M] = 0.0;
+#pragma unroll
+    for (int pass = 0; pass < 2; ++pass)
+#pragma unroll
+      for (int j = M - 1; j >= 1; --j) two_sum(f[j - 1], f[j], f[j - 1], f[j]);
+    return renorm<M>(f);
+  }
 };
 template <>
 struct Acc<2> {
@@ -456,12 +517,36 @@ struct Acc<2> {
     two_sum(hi, p, hi, t);
     lo = __dadd_rn(lo, __dadd_rn(t, pe));
   }
+  __device__ __forceinline__ void renorm_bins() { two_sum(hi, lo, hi, lo); }
+  __device__ __forceinline__ void merge(const Acc& o) {
+    double t;
+    two_sum(hi, o.hi, hi, t);
+    lo = __dadd_rn(lo, __dadd_rn(o.lo, t));
+  }
+  static constexpr int NV = 2;
+  __device__ __forceinline__ double& r(int i) { return i == 0 ? hi : lo; }
+  __device__ __forceinline__ double r(int i) const { return i == 0 ? hi : lo; }
   __device__ __forceinline__ md<2> get() const {
     md<2> r;
     two_sum(hi, lo, r.v[0], r.v[1]);
     return r;
   }
 };
+
+template <int M>
+__device__ __forceinline__ Acc<M> acc_shfl_xor(const Acc<M>& a, int m) {
+  Acc<M> o;
+#pragma unroll
+  for (int k = 0; k < Acc<M>::NV; ++k) o.r(k) = __shfl_xor_sync(0xffffffffu, a.r(k), m);
+  return o;
+}
+template <int M>
+__device__ __forceinline__ Acc<M> acc_shfl_down(const Acc<M>& a, int d) {
+  Acc<M> o;
+#pragma unroll
+  for (int k = 0; k < Acc<M>::NV; ++k) o.r(k) = __shfl_down_sync(0xffffffffu, a.r(k), d);
+  return o;
+}
 
 // ----------------------------------------------------------------------------
 // limb-planar access: limb k of element e at p[k*ps + e]

@@ -4,6 +4,7 @@
 #include <cstdlib>
 #include <vector>
 
+#define MDLS_LEAF_SMEM_TU
 #include "../paper_2110_08375_b200/csrc/kern_leaf.cuh"
 
 namespace mdls {
