@@ -434,6 +434,49 @@ struct HalveAcc<M, V, 0, TPR> {
   static constexpr int V_END = V;
 };
 
+// --- async DSMEM helpers (st.async + mbarrier complete_tx) ---
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t cluster_addr(uint32_t a, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_async_v2(uint32_t raddr, double x, double y, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];"
+               :: "r"(raddr), "d"(x), "d"(y), "r"(rbar) : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arm(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "MDLS_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra MDLS_WAIT_%=;\n}\n" :: "r"(bar), "r"(parity) : "memory");
+}
+// push an md-like value of NV doubles (NV even) to the same smem slot of CTA `rank`
+template <int NV>
+__device__ __forceinline__ void push_vals(const double* v, const void* local_slot, int rank, uint32_t local_bar) {
+  const uint32_t ra = cluster_addr(smem_addr(local_slot), rank);
+  const uint32_t rb = cluster_addr(local_bar, rank);
+#pragma unroll
+  for (int k = 0; k < NV; k += 2) st_async_v2(ra + 8 * k, v[k], v[k + 1], rb);
+}
+
+// t - v w through the level-bin accumulator (one normalisation)
+template <int M>
+__device__ __forceinline__ md<M> fms_acc(const md<M>& t, const md<M>& v, const md<M>& w) {
+  Acc<M> a;
+#pragma unroll
+  for (int k = 0; k < Acc<M>::NV; ++k) a.r(k) = (k < M) ? t.v[k] : 0.0;
+  a.add_prod(neg(v), w);
+  return a.get();
+}
+
 template <int M, int B, int TPR, int NT>
 __global__ void __launch_bounds__(NT) leaf_reg_kernel(LeafArgs<M> a) {
   constexpr int V = B / TPR;
@@ -441,7 +484,8 @@ __global__ void __launch_bounds__(NT) leaf_reg_kernel(LeafArgs<M> a) {
   constexpr int CMAX = 16;
   constexpr int GS = 16;  // lanes per column in the final partial sum
   static_assert(V >= 1 && B % TPR == 0 && 32 % TPR == 0, "leaf shape");
-  static_assert(B * NW <= NT && 32 % NW == 0 && NW >= 4 && B * GS <= NT, "leaf threads");
+  static_assert(B * NW <= NT && 32 % NW == 0 && NW >= 4 && B * GS <= NT && (B * NW) % 32 == 0, "leaf threads");
+  static_assert(M % 2 == 0, "pushes move pairs of doubles");
 
   cg::cluster_group cluster = cg::this_cluster();
   const int C = (int)cluster.num_blocks();
@@ -449,14 +493,15 @@ __global__ void __launch_bounds__(NT) leaf_reg_kernel(LeafArgs<M> a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int h = tid % TPR, rg = tid / TPR;
 
-  __shared__ Acc<M> red[2][CMAX][B];  // pushed CTA partials [buffer][source rank][column]
-  __shared__ md<M> piv[2][B];         // pushed pivot row
-  __shared__ md<M> pvl[B];            // pivot row staging in the owner CTA
+  __shared__ __align__(16) Acc<M> red[2][CMAX][B];  // pushed CTA partials [buffer][source rank][column]
+  __shared__ __align__(16) md<M> piv[2][B];         // pushed pivot row
+  __shared__ __align__(16) md<M> pvl[B];            // pivot row staging in the owner CTA
+  __shared__ __align__(8) unsigned long long bar[2];
   __shared__ Acc<M> wpart[NW][B];
-  __shared__ md<M> G[B], betas[B];
+  __shared__ md<M> G[B], W[B], betas[B];
   __shared__ md<M> SY[B][B];  // SY[p][l] = Y_p^T v_l (p < l)
   __shared__ md<M> Ts[B][B];
-  __shared__ md<M> sc_mu, sc_rs, sc_rsig, sc_rmu;
+  __shared__ md<M> sc_mu, sc_rs, sc_rsig, sc_rmu, sc_rv1;
 
   const int64_t total = a.Mrows - a.js;
   const int64_t row0 = a.js + (int64_t)rank * a.R;
@@ -464,7 +509,15 @@ __global__ void __launch_bounds__(NT) leaf_reg_kernel(LeafArgs<M> a) {
   Rp = Rp < 0 ? 0 : (Rp > a.R ? a.R : Rp);
   const bool valid = rg < Rp;
   const int64_t gi = row0 + rg;
+  const uint32_t tx_bytes = (uint32_t)(C * B * sizeof(Acc<M>) + B * sizeof(md<M>));
 
+  if (tid == 0) {
+    mbar_init(smem_addr(&bar[0]), 1);
+    mbar_init(smem_addr(&bar[1]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_arm(smem_addr(&bar[0]), tx_bytes);
+    if (B > 1) mbar_arm(smem_addr(&bar[1]), tx_bytes);
+  }
   md<M> t[V];
 #pragma unroll
   for (int q = 0; q < V; ++q) {
@@ -472,6 +525,7 @@ __global__ void __launch_bounds__(NT) leaf_reg_kernel(LeafArgs<M> a) {
 #pragma unroll
     for (int k = 0; k < M; ++k) t[q].v[k] = valid ? a.A.p[k * a.A.ps + (a.js + c) * a.A.ld + gi] : 0.0;
   }
+  cluster.sync();  // every CTA's barriers initialised and armed before the first push
 
   for (int l = 0; l < B; ++l) {
     const int64_t j = a.js + l;
@@ -496,7 +550,7 @@ __global__ void __launch_bounds__(NT) leaf_reg_kernel(LeafArgs<M> a) {
       for (int q = 0; q < V; ++q) pvl[h * V + q] = t[q];
     }
     LEAF_MARK(l, 1);
-    // (2) warp reduce-scatter, cross-warp sum, push to every CTA
+    // (2) warp reduce-scatter, cross-warp sum, async push to every CTA
     int base = 0, plain = 0;
     HalveAcc<M, V, 16, TPR>::run(acc, lane, base, plain);
     constexpr int VE = HalveAcc<M, V, 16, TPR>::V_END;
@@ -505,6 +559,7 @@ __global__ void __launch_bounds__(NT) leaf_reg_kernel(LeafArgs<M> a) {
       for (int q = 0; q < VE; ++q) wpart[warp][h * V + base + q] = acc[q];
     }
     __syncthreads();
+    const uint32_t lbar = smem_addr(&bar[buf]);
     if (tid < B * NW) {
       const int c = tid / NW, w = tid % NW;
       Acc<M> s = wpart[w][c];
@@ -513,24 +568,21 @@ __global__ void __launch_bounds__(NT) leaf_reg_kernel(LeafArgs<M> a) {
         Acc<M> o = acc_shfl_down<M>(s, d);
         if (w + d < NW) s.merge(o);
       }
-      // broadcast the CTA sum to the NW lanes of this column, which push it
+      double sv[Acc<M>::NV];
 #pragma unroll
-      for (int k = 0; k < Acc<M>::NV; ++k) s.r(k) = __shfl_sync(0xffffffffu, s.r(k), (lane & ~(NW - 1)));
-      for (int q = w; q < C; q += NW) *cluster.map_shared_rank(&red[buf][rank][c], q) = s;
-    }
-    if (rank == p_piv) {
-      for (int e = tid; e < B * C; e += NT) {
+      for (int k = 0; k < Acc<M>::NV; ++k) sv[k] = __shfl_sync(0xffffffffu, s.r(k), (lane & ~(NW - 1)));
+      for (int q = w; q < C; q += NW) push_vals<Acc<M>::NV>(sv, &red[buf][rank][c], q, lbar);
+    } else if (rank == p_piv) {
+      for (int e = tid - B * NW; e < B * C; e += NT - B * NW) {
         const int c = e % B, q = e / B;
-        *cluster.map_shared_rank(&piv[buf][c], q) = pvl[c];
+        push_vals<M>(pvl[c].v, &piv[buf][c], q, lbar);
       }
     }
     LEAF_MARK(l, 2);
-    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
-    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-    LEAF_MARK(l, 3);
-
-    // (3) fixed-order sum of the C partials (local smem), GS lanes per column
+    // (3) wait for the C partials and the pivot row; fixed-order sum, GS lanes per column
     if (tid < B * GS) {
+      mbar_wait(lbar, (uint32_t)((l >> 1) & 1));
+      LEAF_MARK(l, 3);
       const int c = tid / GS, q = tid % GS;
       Acc<M> s;
       if (q < C) s = red[buf][q][c];
@@ -541,6 +593,7 @@ __global__ void __launch_bounds__(NT) leaf_reg_kernel(LeafArgs<M> a) {
         if (q + d < GS) s.merge(o);
       }
       if (q == 0) G[c] = s.get();
+      if (tid == 0 && l + 2 < B) mbar_arm(lbar, tx_bytes);
     }
     __syncthreads();
     LEAF_MARK(l, 4);
@@ -578,42 +631,45 @@ __global__ void __launch_bounds__(NT) leaf_reg_kernel(LeafArgs<M> a) {
     }
     __syncthreads();
     LEAF_MARK(l, 5);
-    const md<M> mu = sc_mu;
-    md<M> beta, rv1;
-    if (deg) {
-      beta = md_zero<M>();
-      rv1 = md_from<M>(1.0);
-    } else if (pos) {
-      rv1 = neg(mul<M>(add<M>(x1, mu), sc_rsig));
-      beta = mul<M>(mul<M>(sigma, sc_rs), sc_rmu);
-    } else {
-      rv1 = sc_rs;
-      beta = neg(mul<M>(sub<M>(x1, mu), sc_rmu));
-    }
+    // (5) beta, 1/v1 and the row w_c = beta (a_jc + g_c / v1) once per column (B threads)
     if (tid < B) {
       const int c = tid;
+      const md<M> mu = sc_mu;
+      md<M> beta, rv1;
+      if (deg) {
+        beta = md_zero<M>();
+        rv1 = md_from<M>(1.0);
+      } else if (pos) {
+        rv1 = neg(mul<M>(add<M>(x1, mu), sc_rsig));
+        beta = mul<M>(mul<M>(sigma, sc_rs), sc_rmu);
+      } else {
+        rv1 = sc_rs;
+        beta = neg(mul<M>(sub<M>(x1, mu), sc_rmu));
+      }
+      if (c == 0) sc_rv1 = rv1;
       if (c < l) SY[c][l] = deg ? piv[buf][c] : add<M>(piv[buf][c], mul<M>(rv1, G[c]));
       else if (c == l) betas[l] = beta;
+      else W[c] = deg ? md_zero<M>() : mul<M>(beta, add<M>(piv[buf][c], mul<M>(rv1, G[c])));
     }
+    __syncthreads();
     LEAF_MARK(l, 6);
     LEAF_MARK(l, 7);
-    // (5) update the own row: t_c -= v_i w_c (c > l), w_c = beta (a_jc + rv1 g_c); column l <- v
+    // (6) update the own row: t_c -= v_i w_c (c > l); column l <- v (mu on the pivot row)
     if (valid && gi >= j) {
       const bool piv_row = gi == j;
-      const md<M> v = piv_row ? md_from<M>(1.0) : (deg ? x : mul<M>(x, rv1));
+      const md<M> v = piv_row ? md_from<M>(1.0) : (deg ? x : mul<M>(x, sc_rv1));
 #pragma unroll
       for (int q = 0; q < V; ++q) {
         const int c = h * V + q;
         if (c > l && !deg) {
-          const md<M> w = mul<M>(beta, add<M>(piv[buf][c], mul<M>(rv1, G[c])));
-          t[q] = piv_row ? sub<M>(t[q], w) : fms<M>(t[q], v, w);
+          t[q] = piv_row ? sub<M>(t[q], W[c]) : fms_acc<M>(t[q], v, W[c]);
         } else if (c == l) {
-          t[q] = piv_row ? mu : v;
+          t[q] = piv_row ? sc_mu : v;
         }
       }
     }
     if (tid == 0 && rank == 0) {
-      const double m0 = mu.v[0];
+      const double m0 = sc_mu.v[0];
       if (!(m0 != 0.0) || !isfinite(m0)) atomicMin(a.info, (int)(j + 1));
     }
     LEAF_MARK(l, 8);
@@ -651,7 +707,7 @@ __global__ void __launch_bounds__(NT) leaf_reg_kernel(LeafArgs<M> a) {
     if (r % C != rank) continue;
     st<M>(a.T.p, a.T.ps, r + (int64_t)c * a.T.ld, (r <= c) ? Ts[r][c] : md_zero<M>());
   }
-  cluster.sync();  // keep every CTA's shared memory alive until all DSMEM traffic is done
+  cluster.sync();  // no CTA exits while another may still push into it
 }
 
 template <int M, int B, int TPR, int NT>

@@ -390,7 +390,16 @@ template <int M>
 __device__ __noinline__ md<M> sqrt_fast(const md<M>& a) {
   if (a.v[0] == 0.0) return md_zero<M>();
   if constexpr (M == 2) {
-    return dd_sqrt(a);  // QDlib's dd sqrt is already the Karp form
+    // Karp: sqrt(a) = a x + x (a - (a x)^2) / 2 with x = rsqrt(a0) (hardware-seeded double);
+    // a0 - p is exact (Sterbenz), so the residual needs three plain operations
+    const double x = ::rsqrt(a.v[0]);
+    const double ax = __dmul_rn(a.v[0], x);
+    double p, e;
+    two_prod(ax, ax, p, e);
+    const double d = __dadd_rn(__dsub_rn(__dsub_rn(a.v[0], p), e), a.v[1]);
+    md<2> c;
+    two_sum(ax, __dmul_rn(d, __dmul_rn(x, 0.5)), c.v[0], c.v[1]);
+    return c;
   } else {
   constexpr int H = M / 2;
   const md<H> yh = rsqrt_to<H, M>(a);

@@ -63,7 +63,9 @@ void run(int Mrows, int bmax) {
 int main() {
   run<2>(1024, 16);
   run<2>(1024, 8);
+  run<2>(512, 16);
+  run<2>(256, 16);
   run<4>(1024, 8);
-  run<8>(1024, 8);
+  // run<8>(1024, 8);  (od: long compile)
   return 0;
 }
