@@ -50,6 +50,9 @@ def build(force: bool = False, verbose: bool = False, extra: list[str] | None = 
     for s in SOURCES:
         src = os.path.join(CSRC, s)
         obj = os.path.join(BUILD, s.replace(".cu", ".o"))
+        only = os.environ.get("MDLS_BUILD_ONLY")  # dev iteration: recompile one precision, link the rest as built
+        if only and os.path.exists(obj) and not (s.endswith(f"_{only}.cu") or s == "ledger.cu"):
+            continue
         if force or _stale(obj, src):
             cmd = [nvcc, *NVCC_FLAGS, *(extra or []), "-c", src, "-o", obj]
             if verbose:

@@ -411,8 +411,9 @@ struct HalveAcc {
           Acc<M> send, keep;
 #pragma unroll
           for (int k = 0; k < Acc<M>::NV; ++k) {
-            send.r(k) = up ? v[q].r(k) : v[q + half].r(k);
-            keep.r(k) = up ? v[q + half].r(k) : v[q].r(k);
+            const double lo_k = v[q].r(k), hi_k = v[q + half].r(k);  // values, not addresses
+            send.r(k) = up ? lo_k : hi_k;
+            keep.r(k) = up ? hi_k : lo_k;
           }
           keep.merge(acc_shfl_xor<M>(send, MASK));
           v[q] = keep;
@@ -535,9 +536,13 @@ __global__ void __launch_bounds__(NT) leaf_reg_kernel(LeafArgs<M> a) {
 
     LEAF_MARK(l, 0);
     // (1) x_i from the row's owner lane of column l; products over the own row
-    md<M> x;
+    md<M> x = t[0];  // column l of the own row (static register selects, no local memory)
 #pragma unroll
-    for (int k = 0; k < M; ++k) x.v[k] = __shfl_sync(0xffffffffu, t[ql].v[k], (lane & ~(TPR - 1)) + hl);
+    for (int q = 1; q < V; ++q)
+#pragma unroll
+      for (int k = 0; k < M; ++k) x.v[k] = (q == ql) ? t[q].v[k] : x.v[k];
+#pragma unroll
+    for (int k = 0; k < M; ++k) x.v[k] = __shfl_sync(0xffffffffu, x.v[k], (lane & ~(TPR - 1)) + hl);
     const bool below = valid && gi > j;
     Acc<M> acc[V];
 #pragma unroll
@@ -600,22 +605,54 @@ __global__ void __launch_bounds__(NT) leaf_reg_kernel(LeafArgs<M> a) {
 
     // (4) Householder scalars (GVL Alg. 5.1.1 with independent reciprocals):
     //   x1 > 0:  s = x1 + mu, 1/v1 = -s/sigma, beta = sigma/(mu s)
-    //   x1 <= 0: v1 = x1 - mu, beta = -v1/mu
+    //   x1 <= 0: v1 = x1 - mu (= s), beta = -v1/mu
+    // then u_c = a_jc + g_c/v1 for every column: Y_c^T v (c < l) and w_c = beta u_c (c > l).
     const md<M> sigma = G[l], x1 = piv[buf][l];
     const bool deg = sigma.v[0] == 0.0;
     const bool pos = x1.v[0] > 0.0;
-    if (!deg) {
-      if (tid == 0) {
-        const md<M> mu = sqrt_fast<M>(add<M>(mul<M>(x1, x1), sigma));
-        sc_mu = mu;
-        sc_rs = recip_fast<M>(pos ? add<M>(x1, mu) : sub<M>(x1, mu));
-      } else if (tid == 32) {
-        if (pos) sc_rsig = recip_fast<M>(sigma);
-      } else if (tid == 64) {
-        sc_rmu = rsqrt_md<M>(add<M>(mul<M>(x1, x1), sigma));
+    if constexpr (M == 2) {
+      // double double: warp 0 computes the three independent chains inline (ILP), no extra barrier
+      if (warp == 0) {
+        md<2> mu = x1, beta = md_zero<2>(), rv1 = md_from<2>(1.0);
+        if (!deg) {
+          const md<2> aa = dd_add(dd_mul(x1, x1), sigma);
+          const double y0 = ::rsqrt(aa.v[0]);
+          mu = dd_sqrt_seeded(aa, y0);
+          const md<2> rmu = dd_rsqrt_seeded(aa, y0);
+          const md<2> sv = pos ? dd_add(x1, mu) : dd_add(x1, neg(mu));
+          const md<2> rs = dd_recip_inl(sv);
+          const md<2> rsig = dd_recip_inl(sigma);
+          rv1 = pos ? neg(dd_mul(sv, rsig)) : rs;
+          beta = pos ? dd_mul(dd_mul(sigma, rs), rmu) : neg(dd_mul(sv, rmu));
+        }
+        if (lane < B) {
+          const int c = lane;
+          const md<2> pc = piv[buf][c];
+          const md<2> u = deg ? pc : dd_add(pc, dd_mul(rv1, G[c]));
+          const md<2> w = dd_mul(beta, u);
+          if (c < l) SY[c][l] = u;
+          else if (c > l) W[c] = w;
+        }
+        if (lane == 0) {
+          sc_mu = mu;
+          sc_rv1 = rv1;
+          betas[l] = beta;
+        }
       }
-    } else if (tid == 0) {
-      sc_mu = x1;
+    } else {
+      if (!deg) {
+        if (tid == 0) {
+          const md<M> mu = sqrt_fast<M>(add<M>(mul<M>(x1, x1), sigma));
+          sc_mu = mu;
+          sc_rs = recip_fast<M>(pos ? add<M>(x1, mu) : sub<M>(x1, mu));
+        } else if (tid == 32) {
+          if (pos) sc_rsig = recip_fast<M>(sigma);
+        } else if (tid == 64) {
+          sc_rmu = rsqrt_md<M>(add<M>(mul<M>(x1, x1), sigma));
+        }
+      } else if (tid == 0) {
+        sc_mu = x1;
+      }
     }
     if (warp == 3 && l > 0) {  // extend this CTA's rows of the leaf T by column l-1
       const int ll = l - 1;
@@ -631,40 +668,47 @@ __global__ void __launch_bounds__(NT) leaf_reg_kernel(LeafArgs<M> a) {
     }
     __syncthreads();
     LEAF_MARK(l, 5);
-    // (5) beta, 1/v1 and the row w_c = beta (a_jc + g_c / v1) once per column (B threads)
-    if (tid < B) {
-      const int c = tid;
-      const md<M> mu = sc_mu;
-      md<M> beta, rv1;
-      if (deg) {
-        beta = md_zero<M>();
-        rv1 = md_from<M>(1.0);
-      } else if (pos) {
-        rv1 = neg(mul<M>(add<M>(x1, mu), sc_rsig));
-        beta = mul<M>(mul<M>(sigma, sc_rs), sc_rmu);
-      } else {
-        rv1 = sc_rs;
-        beta = neg(mul<M>(sub<M>(x1, mu), sc_rmu));
+    if constexpr (M != 2) {
+      // (5) beta, 1/v1 and u_c / w_c once per column (B threads, no divergent arithmetic)
+      if (tid < B) {
+        const int c = tid;
+        const md<M> mu = sc_mu;
+        md<M> beta, rv1;
+        if (deg) {
+          beta = md_zero<M>();
+          rv1 = md_from<M>(1.0);
+        } else if (pos) {
+          rv1 = neg(mul<M>(add<M>(x1, mu), sc_rsig));
+          beta = mul<M>(mul<M>(sigma, sc_rs), sc_rmu);
+        } else {
+          rv1 = sc_rs;
+          beta = neg(mul<M>(sub<M>(x1, mu), sc_rmu));
+        }
+        if (c == 0) sc_rv1 = rv1;
+        const md<M> pc = piv[buf][c];
+        const md<M> u = deg ? pc : add<M>(pc, mul<M>(rv1, G[c]));
+        const md<M> w = mul<M>(beta, u);
+        if (c < l) SY[c][l] = u;
+        else if (c == l) betas[l] = beta;
+        else W[c] = w;
       }
-      if (c == 0) sc_rv1 = rv1;
-      if (c < l) SY[c][l] = deg ? piv[buf][c] : add<M>(piv[buf][c], mul<M>(rv1, G[c]));
-      else if (c == l) betas[l] = beta;
-      else W[c] = deg ? md_zero<M>() : mul<M>(beta, add<M>(piv[buf][c], mul<M>(rv1, G[c])));
+      __syncthreads();
     }
-    __syncthreads();
     LEAF_MARK(l, 6);
     LEAF_MARK(l, 7);
-    // (6) update the own row: t_c -= v_i w_c (c > l); column l <- v (mu on the pivot row)
+    // (6) update the own row: t_c -= v_i w_c (c > l, v = 1 on the pivot row); column l <- v (mu on the pivot row)
     if (valid && gi >= j) {
       const bool piv_row = gi == j;
       const md<M> v = piv_row ? md_from<M>(1.0) : (deg ? x : mul<M>(x, sc_rv1));
+      const md<M> mu = sc_mu;
 #pragma unroll
       for (int q = 0; q < V; ++q) {
         const int c = h * V + q;
         if (c > l && !deg) {
-          t[q] = piv_row ? sub<M>(t[q], W[c]) : fms_acc<M>(t[q], v, W[c]);
+          t[q] = fms_acc<M>(t[q], v, W[c]);
         } else if (c == l) {
-          t[q] = piv_row ? sc_mu : v;
+#pragma unroll
+          for (int k = 0; k < M; ++k) t[q].v[k] = piv_row ? mu.v[k] : v.v[k];
         }
       }
     }

@@ -435,6 +435,37 @@ __device__ __noinline__ md<M> recip_fast(const md<M>& d) {
   }
 }
 
+// inline double-double pieces for the panel's scalar chain (dd only; the
+// generic sqrt_fast / recip_fast are out-of-line)
+// sqrt(a) by Karp from a double seed y0 ~ 1/sqrt(a0)
+__device__ __forceinline__ md<2> dd_sqrt_seeded(const md<2>& a, double y0) {
+  const double ax = __dmul_rn(a.v[0], y0);
+  double p, e;
+  two_prod(ax, ax, p, e);
+  const double d = __dadd_rn(__dsub_rn(__dsub_rn(a.v[0], p), e), a.v[1]);
+  md<2> c;
+  two_sum(ax, __dmul_rn(d, __dmul_rn(y0, 0.5)), c.v[0], c.v[1]);
+  return c;
+}
+// 1/sqrt(a): one Newton step y0 + y0 (1 - a y0^2) / 2 with the residual in double double
+__device__ __forceinline__ md<2> dd_rsqrt_seeded(const md<2>& a, double y0) {
+  double p, e;
+  two_prod(y0, y0, p, e);                                   // y0^2 exactly
+  const md<2> q = dd_mul(a, md<2>{{p, e}});                 // a y0^2
+  const double r = __dadd_rn(__dsub_rn(1.0, q.v[0]), -q.v[1]);  // 1 - a y0^2 (tiny; Sterbenz)
+  md<2> c;
+  two_sum(y0, __dmul_rn(__dmul_rn(y0, 0.5), r), c.v[0], c.v[1]);
+  return c;
+}
+// 1/d: y0 = rcp(d0), y = y0 + y0 (1 - d y0)
+__device__ __forceinline__ md<2> dd_recip_inl(const md<2>& d) {
+  const double y0 = __drcp_rn(d.v[0]);
+  const double r = __fma_rn(-d.v[1], y0, __fma_rn(-d.v[0], y0, 1.0));  // 1 - d y0 (first fma exact)
+  md<2> c;
+  two_sum(y0, __dmul_rn(y0, r), c.v[0], c.v[1]);
+  return c;
+}
+
 // ----------------------------------------------------------------------------
 // dot-product accumulator: sum_k a_k * b_k.  Generic precisions keep a
 // renormalised md sum (one md mul + one md add per term, 267 / 1471 FP64 ops

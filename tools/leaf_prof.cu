@@ -65,7 +65,9 @@ int main() {
   run<2>(1024, 8);
   run<2>(512, 16);
   run<2>(256, 16);
+#ifdef PROF_QD
   run<4>(1024, 8);
+#endif
   // run<8>(1024, 8);  (od: long compile)
   return 0;
 }
