@@ -44,6 +44,18 @@ inline bool q_forward() {
   return v == 1;
 }
 
+// chained-leaf factorisation (solver.cuh::qr_factor_chain) where every leaf fits the register
+// leaf; MDLS_CHAIN=0 forces the GEMM-chained panel path
+template <int MM>
+inline bool use_chain(int64_t Mr, int64_t K, int64_t nb) {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MDLS_CHAIN");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1 && chain_supported<MM>(Mr, K, nb);
+}
+
 inline int tile_ok(int64_t Mr, int64_t K, int64_t nb) {
   if (K < 1) return -2;
   if (Mr < K) return -1;
@@ -162,9 +174,14 @@ int MDLS_FN(mdls_qr_)(int64_t Mr, int64_t K, int64_t nb, double* A, int64_t lda,
   Mat Am{A, lda, psa};
   Mat Qm{Q, ldq, psq};
   const bool fwd = Q && q_forward<M>();
-  if (qr_factor_overlap<M>(b.lane(0, st), b.lane(1, side_stream(0)), b.lane(2, side_stream(1)), Mr, K, nb, Am, b,
-                           fwd ? &Qm : nullptr) != cudaSuccess)
+  if (use_chain<M>(Mr, K, nb)) {
+    if (qr_factor_chain<M>(st, Mr, K, nb, Am, b, Mat{at<double>(work, p.wl), Mr, Mr * K},
+                           Mat{at<double>(work, p.t), 32, 32 * std::max<int64_t>(K, 32)}, fwd ? &Qm : nullptr) != cudaSuccess)
+      return MDLS_ERR_CUDA;
+  } else if (qr_factor_overlap<M>(b.lane(0, st), b.lane(1, side_stream(0)), b.lane(2, side_stream(1)), Mr, K, nb, Am,
+                                  b, fwd ? &Qm : nullptr) != cudaSuccess) {
     return MDLS_ERR_CUDA;
+  }
   if (Q && !fwd) form_q_backward<M>(st, Mr, K, nb, Qm, b);
   if (dev_info) MDLS_LAUNCH(F_MISC, st, info_finish_kernel<<<1, 1, 0, st>>>(b.info_slot, nullptr, dev_info));
   return launched();
@@ -241,9 +258,14 @@ int MDLS_FN(mdls_lstsq_)(int64_t Mr, int64_t K, int64_t nb, const double* A, int
   cudaMemsetAsync(bb.W.p, 0, sizeof(double) * M * Mr * K, st);
   Mat Q = (form_q && Q_out) ? Mat{Q_out, ldq, psq} : Mat{form_q ? at<double>(work, p.q) : nullptr, Mr, Mr * Mr};
   const bool fwd = form_q && q_forward<M>();
-  if (qr_factor_overlap<M>(bb.lane(0, st), bb.lane(1, side_stream(0)), bb.lane(2, side_stream(1)), Mr, K, nb, Af, bb,
-                           fwd ? &Q : nullptr) != cudaSuccess)
+  if (use_chain<M>(Mr, K, nb)) {
+    if (qr_factor_chain<M>(st, Mr, K, nb, Af, bb, Mat{at<double>(work, p.wl), Mr, Mr * K},
+                           Mat{at<double>(work, p.t), 32, 32 * std::max<int64_t>(K, 32)}, fwd ? &Q : nullptr) != cudaSuccess)
+      return MDLS_ERR_CUDA;
+  } else if (qr_factor_overlap<M>(bb.lane(0, st), bb.lane(1, side_stream(0)), bb.lane(2, side_stream(1)), Mr, K, nb,
+                                  Af, bb, fwd ? &Q : nullptr) != cudaSuccess) {
     return MDLS_ERR_CUDA;
+  }
   double* yv = at<double>(work, p.v1);
   if (form_q) {
     if (!fwd) form_q_backward<M>(st, Mr, K, nb, Q, bb);

@@ -17,7 +17,7 @@
 // compact-WY factor T (T_ll = beta_l, T(:l, l) = -beta_l T(:l,:l) Y(:,:l)^T v_l,
 // which is the paper's z = -beta (v + W Y^T v), with W = -Y T).
 #pragma once
-#include "types.cuh"
+#include "launch.cuh"
 
 namespace mdls {
 
@@ -32,6 +32,11 @@ struct LeafArgs {
   int64_t bps;
   Mat T;          // B x B leaf T (upper triangular, zeros below)
   int* info;      // min-slot: 1-based first zero / non-finite R_jj
+  // register leaf only: apply the previous leaf (columns jsp..jsp+B-1, same width) to this
+  // leaf's columns first, C -= Yp Tp^T (Yp^T C) on rows jsp..Mrows-1 (jsp < 0: none)
+  Mat Yp;         // explicit Y (global column indexing, as Y)
+  Mat Tp;         // previous leaf's T (B x B, upper)
+  int64_t jsp;
 };
 
 // Reduce-scatter sum of V md values over the lanes of a warp that share
@@ -478,6 +483,200 @@ __device__ __forceinline__ md<M> fms_acc(const md<M>& t, const md<M>& v, const m
   return a.get();
 }
 
+// ---------------------------------------------------------------------------
+// Prologue of the chained register leaf: apply the previous leaf's block
+// reflector to this leaf's B columns (the "beta R^T v" + "update R" work of the
+// panel, for the one block the chain waits on):
+//     C <- C - Yp Tp^T (Yp^T C)      rows jsp..M-1 (P_WY = I + W Y^T, W = -Y T)
+// Z = Yp^T C is reduced over the cluster by reduce-scatter (column c of Z to
+// CTA c mod C, async pushes + mbarrier), the owner forms Z'(:,c) = Tp^T Z(:,c)
+// and pushes it to every CTA, and each CTA updates its rows (CTA 0 also the B
+// rows jsp..js-1 above the leaf, which become rows of R).  Shared memory
+// (dynamic): Ys, Cs [RX][B] md, zred [CMAX][2][B] Acc, Zp [B][B] md.
+// ---------------------------------------------------------------------------
+template <int M, int B, int NT>
+struct LeafPro {
+  static constexpr int RX = ((NT / 4 + B) + 63) / 64 * 64;  // rows staged per CTA (tile rows + the B rows above), padded
+  static constexpr int BP = B + 1;  // padded row stride (no bank conflicts across rows)
+  static constexpr size_t ys = 0, cs = sizeof(md<M>) * RX * BP, zr = 2 * cs;
+  static constexpr size_t zp = zr + sizeof(Acc<M>) * 16 * 2 * B;
+  static constexpr size_t tp = zp + sizeof(md<M>) * B * B;
+  static constexpr size_t zs = tp + sizeof(md<M>) * B * B;
+  static constexpr size_t bytes = zs + sizeof(md<M>) * 2 * B;
+};
+
+template <int M, int B, int TPR, int NT>
+__device__ __forceinline__ void leaf_prologue(const LeafArgs<M>& a, cg::cluster_group& cluster, int C, int rank,
+                                              md<M> (&t)[B / TPR], int64_t Rp, bool valid, int64_t gi, int64_t row0) {
+  using P = LeafPro<M, B, NT>;
+  constexpr int BP = P::BP;
+  constexpr int V = B / TPR;
+  constexpr int BB = B * B;
+  constexpr int RS = (NT / BB) >= 1 ? NT / BB : 1;  // lanes per Z entry (row split)
+  static_assert(NT % BB == 0 || BB % NT == 0, "prologue threads");
+  extern __shared__ __align__(16) unsigned char leaf_dyn[];
+  md<M>* Ys = reinterpret_cast<md<M>*>(leaf_dyn + P::ys);
+  md<M>* Cs = reinterpret_cast<md<M>*>(leaf_dyn + P::cs);
+  Acc<M>* zred = reinterpret_cast<Acc<M>*>(leaf_dyn + P::zr);  // [src][cc][p]
+  md<M>* Zp = reinterpret_cast<md<M>*>(leaf_dyn + P::zp);      // [p][c]
+  md<M>* Tsm = reinterpret_cast<md<M>*>(leaf_dyn + P::tp);     // [pp][p] = Tp(p, pp)
+  md<M>* Zsum = reinterpret_cast<md<M>*>(leaf_dyn + P::zs);    // [cc][p] summed Z(:, c)
+  __shared__ __align__(8) unsigned long long zbar[2];
+  const int tid = threadIdx.x, lane = tid & 31;
+  // the B rows above the leaf (jsp..js-1) are spread over the CTAs: row jsp + rank + k C, k < ex
+  const int ex = (rank < B) ? (B - 1 - rank) / C + 1 : 0;
+  const int Rx = (int)Rp + ex;
+  const int ncol = (B - 1 - rank) / C + 1 > 0 && rank < B ? (B - 1 - rank) / C + 1 : 0;  // owned Z columns
+  if (tid == 0) {
+    mbar_init(smem_addr(&zbar[0]), 1);
+    mbar_init(smem_addr(&zbar[1]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_arm(smem_addr(&zbar[0]), (uint32_t)(C * B * ncol * sizeof(Acc<M>)));
+    mbar_arm(smem_addr(&zbar[1]), (uint32_t)(BB * sizeof(md<M>)));
+  }
+  // stage Yp and C rows: local row i < ex -> global jsp + i, else row0 + (i - ex); zero padding
+  // to a multiple of 4 RS rows so the partial-product loop is branch free
+  constexpr int RS0 = (NT / BB) >= 1 ? NT / BB : 1;
+  const int Rxp = (Rx + 4 * RS0 - 1) / (4 * RS0) * (4 * RS0);
+  for (int e = tid; e < Rxp * B; e += NT) {
+    const int i = e / B, p = e % B;
+    const int64_t g = (i < ex) ? a.jsp + rank + (int64_t)i * C : row0 + (i - ex);
+    md<M> y = md_zero<M>(), c = md_zero<M>();
+    if (i < Rx) {
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+        y.v[k] = a.Yp.p[k * a.Yp.ps + (a.jsp + p) * a.Yp.ld + g];
+        c.v[k] = a.A.p[k * a.A.ps + (a.js + p) * a.A.ld + g];
+      }
+    }
+    Ys[i * BP + p] = y;
+    Cs[i * BP + p] = c;
+  }
+  for (int e = tid; e < BB; e += NT) {
+    const int p = e % B, pp = e / B;
+    md<M> tv;
+#pragma unroll
+    for (int k = 0; k < M; ++k) tv.v[k] = a.Tp.p[k * a.Tp.ps + pp * a.Tp.ld + p];
+    Tsm[e] = tv;
+  }
+  LEAF_MARK(63, 0);
+  cluster.sync();  // barriers armed everywhere, staging visible
+  LEAF_MARK(63, 1);
+  // Z partial (p, c) over the staged rows, RS lanes per entry, 4 interleaved accumulators
+  {
+    const int e = tid / RS, r0 = tid % RS;
+    if (e < BB) {
+      const int p = e % B, c = e / B;
+      Acc<M> acc[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[u].init();
+#pragma unroll 2
+      for (int i = 4 * r0; i < Rxp; i += 4 * RS) {
+        md<M> yv[4], cv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          yv[u] = Ys[(i + u) * BP + p];
+          cv[u] = Cs[(i + u) * BP + c];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[u].add_prod(yv[u], cv[u]);
+      }
+      acc[0].merge(acc[1]);
+      acc[2].merge(acc[3]);
+      acc[0].merge(acc[2]);
+#pragma unroll
+      for (int d = RS / 2; d >= 1; d >>= 1) {
+        Acc<M> o = acc_shfl_down<M>(acc[0], d);
+        if (r0 + d < RS) acc[0].merge(o);
+      }
+      if (r0 == 0) {
+        const int q = c % C, cc = c / C;
+        double sv[Acc<M>::NV];
+#pragma unroll
+        for (int k = 0; k < Acc<M>::NV; ++k) sv[k] = acc[0].r(k);
+        push_vals<Acc<M>::NV>(sv, &zred[(rank * 2 + cc) * B + p], q, smem_addr(&zbar[0]));
+      }
+    }
+  }
+  LEAF_MARK(63, 2);
+  // owner: Z(:, c) = sum of the C partials (fixed order), Z'(:, c) = Tp^T Z(:, c), push to all CTAs
+  if (ncol > 0) {
+    mbar_wait(smem_addr(&zbar[0]), 0);
+    __syncthreads();
+    LEAF_MARK(63, 3);
+    // Z(p, c) = fixed-order tree over the C source partials: thread (cc, p, q), 16 lanes per entry
+    for (int e = tid; e < ncol * B * 16; e += NT) {
+      const int q = e % 16, p = (e / 16) % B, cc = e / (16 * B);
+      Acc<M> z;
+      if (q < C) z = zred[(q * 2 + cc) * B + p];
+      else z.init();
+#pragma unroll
+      for (int d = 8; d >= 1; d >>= 1) {
+        Acc<M> o = acc_shfl_down<M>(z, d);
+        if (q + d < 16) z.merge(o);
+      }
+      if (q == 0) Zsum[cc * B + p] = z.get();
+    }
+    __syncthreads();
+    for (int cc = 0; cc < ncol; ++cc) {
+      const int c = rank + cc * C;
+      // Z'(pp, c) = sum_{p <= pp} Tp(p, pp) Z(p, c): thread (pp, p), B lanes per output
+      if (tid < BB) {
+        const int pp = tid / B, p = tid % B;
+        Acc<M> pr;
+        pr.init();
+        if (p <= pp) pr.add_prod(Tsm[pp * B + p], Zsum[cc * B + p]);
+#pragma unroll
+        for (int d = B / 2; d >= 1; d >>= 1) {
+          Acc<M> o = acc_shfl_down<M>(pr, d);
+          if (p + d < B) pr.merge(o);
+        }
+        const md<M> zz = pr.get();
+        // lanes p < C of each group push to CTA p (parallel pushes)
+        md<M> zb;
+#pragma unroll
+        for (int k = 0; k < M; ++k) zb.v[k] = __shfl_sync(0xffffffffu, zz.v[k], (tid & 31) & ~(B - 1));
+        for (int q = p; q < C; q += B) push_vals<M>(zb.v, &Zp[pp * B + c], q, smem_addr(&zbar[1]));
+      }
+    }
+  }
+  LEAF_MARK(63, 4);
+  mbar_wait(smem_addr(&zbar[1]), 0);
+  __syncthreads();
+  LEAF_MARK(63, 5);
+  // update own rows (registers) and, in CTA 0, the B rows above the leaf (global)
+  if (valid) {
+    const int h = tid % TPR;
+    const int i = ex + (int)(gi - row0);
+    Acc<M> u[V];
+#pragma unroll
+    for (int q = 0; q < V; ++q)
+#pragma unroll
+      for (int k = 0; k < Acc<M>::NV; ++k) u[q].r(k) = (k < M) ? t[q].v[k] : 0.0;
+#pragma unroll 4
+    for (int p = 0; p < B; ++p) {
+      const md<M> y = neg(Ys[i * BP + p]);
+#pragma unroll
+      for (int q = 0; q < V; ++q) u[q].add_prod(y, Zp[p * B + h * V + q]);
+    }
+#pragma unroll
+    for (int q = 0; q < V; ++q) t[q] = u[q].get();
+  }
+  for (int e = tid; e < ex * B; e += NT) {
+    const int i = e / B, c = e % B;
+    Acc<M> u;
+    const md<M> c0 = Cs[i * BP + c];
+#pragma unroll
+    for (int k = 0; k < Acc<M>::NV; ++k) u.r(k) = (k < M) ? c0.v[k] : 0.0;
+    for (int p = 0; p < B; ++p) u.add_prod(neg(Ys[i * BP + p]), Zp[p * B + c]);
+    const md<M> r = u.get();
+#pragma unroll
+    for (int k = 0; k < M; ++k) a.A.p[k * a.A.ps + (a.js + c) * a.A.ld + a.jsp + rank + (int64_t)i * C] = r.v[k];
+  }
+  LEAF_MARK(63, 6);
+  (void)lane;
+}
+
 template <int M, int B, int TPR, int NT>
 __global__ void __launch_bounds__(NT) leaf_reg_kernel(LeafArgs<M> a) {
   constexpr int V = B / TPR;
@@ -526,7 +725,8 @@ __global__ void __launch_bounds__(NT) leaf_reg_kernel(LeafArgs<M> a) {
 #pragma unroll
     for (int k = 0; k < M; ++k) t[q].v[k] = valid ? a.A.p[k * a.A.ps + (a.js + c) * a.A.ld + gi] : 0.0;
   }
-  cluster.sync();  // every CTA's barriers initialised and armed before the first push
+  if (a.jsp >= 0) leaf_prologue<M, B, TPR, NT>(a, cluster, C, rank, t, Rp, valid, gi, row0);
+  else cluster.sync();  // every CTA's barriers initialised and armed before the first push
 
   for (int l = 0; l < B; ++l) {
     const int64_t j = a.js + l;
@@ -631,7 +831,7 @@ __global__ void __launch_bounds__(NT) leaf_reg_kernel(LeafArgs<M> a) {
           const md<2> u = deg ? pc : dd_add(pc, dd_mul(rv1, G[c]));
           const md<2> w = dd_mul(beta, u);
           if (c < l) SY[c][l] = u;
-          else if (c > l) W[c] = w;
+          W[c] = (c > l && !deg) ? w : md_zero<2>();  // zero w: the update below is branch free
         }
         if (lane == 0) {
           sc_mu = mu;
@@ -690,7 +890,7 @@ __global__ void __launch_bounds__(NT) leaf_reg_kernel(LeafArgs<M> a) {
         const md<M> w = mul<M>(beta, u);
         if (c < l) SY[c][l] = u;
         else if (c == l) betas[l] = beta;
-        else W[c] = w;
+        W[c] = (c > l && !deg) ? w : md_zero<M>();
       }
       __syncthreads();
     }
@@ -701,15 +901,14 @@ __global__ void __launch_bounds__(NT) leaf_reg_kernel(LeafArgs<M> a) {
       const bool piv_row = gi == j;
       const md<M> v = piv_row ? md_from<M>(1.0) : (deg ? x : mul<M>(x, sc_rv1));
       const md<M> mu = sc_mu;
+      md<M> nt[V];
+#pragma unroll
+      for (int q = 0; q < V; ++q) nt[q] = fms_acc<M>(t[q], v, W[h * V + q]);  // w = 0 for c <= l: t unchanged
 #pragma unroll
       for (int q = 0; q < V; ++q) {
-        const int c = h * V + q;
-        if (c > l && !deg) {
-          t[q] = fms_acc<M>(t[q], v, W[c]);
-        } else if (c == l) {
+        const bool isl = (h * V + q) == l;
 #pragma unroll
-          for (int k = 0; k < M; ++k) t[q].v[k] = piv_row ? mu.v[k] : v.v[k];
-        }
+        for (int k = 0; k < M; ++k) t[q].v[k] = isl ? (piv_row ? mu.v[k] : v.v[k]) : nt[q].v[k];
       }
     }
     if (tid == 0 && rank == 0) {
@@ -757,11 +956,24 @@ __global__ void __launch_bounds__(NT) leaf_reg_kernel(LeafArgs<M> a) {
 template <int M, int B, int TPR, int NT>
 cudaError_t leaf_reg_launch(cudaStream_t st, const LeafArgs<M>& la, int C) {
   auto kern = leaf_reg_kernel<M, B, TPR, NT>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  // MDLS_LEAF_EXCL=1: request enough shared memory that no other CTA (the concurrent
+  // trailing / Q GEMMs) can share the leaf's SMs and its FP64 pipes
+  static const size_t excl = [] {
+    const char* v = getenv("MDLS_LEAF_EXCL");
+    return (size_t)((v && v[0] == '1') ? 180 * 1024 : 0);
+  }();
+  const size_t dyn = std::max((la.jsp >= 0) ? LeafPro<M, B, NT>::bytes : (size_t)0, excl);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)std::max(LeafPro<M, B, NT>::bytes, (size_t)180 * 1024));
+    attr_set = true;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(C, 1, 1);
   cfg.blockDim = dim3(NT, 1, 1);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = dyn;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -835,7 +1047,7 @@ cudaError_t launch_leaf(cudaStream_t st, int64_t Mrows, int64_t js, int64_t bmax
     const int64_t R = cdiv(rows, C);
     while (B > 1 && leaf_smem_bytes(M, B, R) > cap) B /= 2;
     if (leaf_smem_bytes(M, B, R) > cap) return cudaErrorInvalidValue;
-    LeafArgs<M> la{Mrows, js, R, A, Y, beta, bps, T, info};
+    LeafArgs<M> la{Mrows, js, R, A, Y, beta, bps, T, info, Mat{nullptr, 0, 0}, Mat{nullptr, 0, 0}, -1};
     cudaError_t e;
     static const bool force_smem = [] {
       const char* v = getenv("MDLS_LEAF");
@@ -880,8 +1092,34 @@ cudaError_t launch_leaf(cudaStream_t st, int64_t Mrows, int64_t js, int64_t bmax
   }
 }
 
+// ---------------------------------------------------------------------------
+// chained leaves (whole-factorisation critical path): the register leaf with
+// the previous-leaf prologue.  chain_leaf_width() returns the leaf width the
+// chain uses at column js (0: shape not supported by the register leaf; the
+// caller then runs the GEMM-chained panel path).
+// ---------------------------------------------------------------------------
+template <int M>
+cudaError_t launch_leaf_chain(cudaStream_t st, int64_t Mrows, int64_t js, int B, Mat A, Mat Y, double* beta,
+                              int64_t bps, Mat T, int* info, Mat Tp, int64_t jsp) {
+  const int64_t rows = Mrows - js;
+  const int C = (int)std::max<int64_t>(1, std::min<int64_t>(leaf_cluster_size(), rows));
+  const int64_t R = cdiv(rows, C);
+  LeafArgs<M> la{Mrows, js, R, A, Y, beta, bps, T, info, Y, Tp, jsp};
+  if constexpr (M == 2) {
+    if (R <= 64) return B == 16 ? leaf_reg_launch<M, 16, 4, 256>(st, la, C) : leaf_reg_launch<M, 8, 4, 256>(st, la, C);
+    return B == 16 ? leaf_reg_launch<M, 16, 4, 512>(st, la, C) : leaf_reg_launch<M, 8, 4, 512>(st, la, C);
+  } else if constexpr (M == 4) {
+    if (R <= 64) return leaf_reg_launch<M, 8, 4, 256>(st, la, C);
+    return leaf_reg_launch<M, 8, 4, 512>(st, la, C);
+  } else {
+    return leaf_reg_launch<M, 8, 4, 256>(st, la, C);
+  }
+}
+
 #define MDLS_INSTANTIATE_LEAF(MM)                                                                               \
   template cudaError_t launch_leaf<MM>(cudaStream_t, int64_t, int64_t, int64_t, Mat, Mat, double*, int64_t, Mat, \
-                                       int*, int*);
+                                       int*, int*);                                                                \
+  template cudaError_t launch_leaf_chain<MM>(cudaStream_t, int64_t, int64_t, int, Mat, Mat, double*, int64_t, Mat, \
+                                             int*, Mat, int64_t);
 
 }  // namespace mdls

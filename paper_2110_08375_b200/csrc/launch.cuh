@@ -2,6 +2,8 @@
 // instantiated per precision) in separate translation units so the three
 // precisions and the kernel families compile in parallel.
 #pragma once
+#include <cstdlib>
+
 #include "types.cuh"
 
 namespace mdls {
@@ -13,6 +15,30 @@ void gemm(cudaStream_t st, int64_t m, int64_t n, int64_t k, CMat A, CMat B, Mat 
 template <int M>
 cudaError_t launch_leaf(cudaStream_t st, int64_t Mrows, int64_t js, int64_t bmax, Mat A, Mat Y, double* beta,
                         int64_t bps, Mat T, int* info, int* bw);
+
+// chained leaves (register leaf with the previous-leaf prologue, kern_leaf.cuh)
+inline int leaf_cluster_size() {
+  static const int c = [] {
+    const char* v = getenv("MDLS_LEAF_C");
+    return (v && v[0] == '8') ? 8 : 16;
+  }();
+  return c;
+}
+template <int M>
+inline int chain_leaf_width(int64_t Mrows, int64_t js, int64_t bmax) {
+  int B = 1;
+  while (B * 2 <= bmax && B * 2 <= (M == 2 ? 16 : 8)) B *= 2;
+  if (B < 8) return 0;
+  const int64_t rows = Mrows - js;
+  const int C = (int)std::max<int64_t>(1, std::min<int64_t>(leaf_cluster_size(), rows));
+  const int64_t R = cdiv(rows, C);
+  if (2 * C < B) return 0;
+  if (R <= 64 || (M <= 4 && R <= 128)) return B;
+  return 0;
+}
+template <int M>
+cudaError_t launch_leaf_chain(cudaStream_t st, int64_t Mrows, int64_t js, int B, Mat A, Mat Y, double* beta,
+                              int64_t bps, Mat T, int* info, Mat Tp, int64_t jsp);
 
 template <int M>
 void launch_invert(cudaStream_t st, int64_t ntiles, int64_t nb, CMat U, Mat Vt, double diag_scale, const double* dbeta,

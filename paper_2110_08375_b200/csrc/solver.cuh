@@ -22,7 +22,7 @@ namespace mdls {
 // workspace plan (bytes, 256-aligned segments)
 // ---------------------------------------------------------------------------
 struct Plan {
-  size_t af = 0, q = 0, y = 0, w = 0, beta = 0, s = 0, t = 0, x = 0, part = 0, v0 = 0, v1 = 0, v2 = 0, vt = 0,
+  size_t af = 0, q = 0, y = 0, w = 0, wl = 0, beta = 0, s = 0, t = 0, x = 0, part = 0, v0 = 0, v1 = 0, v2 = 0, vt = 0,
          info = 0, total = 0;
 };
 
@@ -45,7 +45,8 @@ Plan make_plan(int op, int64_t Mr, int64_t K, int64_t nb) {
     p.w = take(md * Mr * K);
     p.beta = take(md * K);
     p.s = take(md * nb * nb);
-    p.t = take(md * std::max<int64_t>(nb * nb, 1024));
+    p.t = take(md * std::max<int64_t>(std::max<int64_t>(nb * nb, 1024), 32 * K));  // leaf T's (ld 32, column js)
+    p.wl = take(md * Mr * K);                                                       // leaf-local W_s = -Y_s T_s
   }
   if (op == MDLS_OP_APPLY_QT) p.y = take(md * Mr * K);
   if (qr_like || op == MDLS_OP_APPLY_QT) {
@@ -204,6 +205,111 @@ cudaError_t qr_factor_overlap(const Lane& L0, const Lane& L1, const Lane& L2, in
   }
   fork(L1.st, L0.st);
   fork(L2.st, L0.st);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Algorithm 2 as a chain of leaves (every leaf a register-leaf cluster kernel
+// that first applies the previous leaf to its own columns).  Streams (all
+// forked from and joined into `st`):
+//   Lc (high priority): the leaves -- the only serial path of the factorisation;
+//   La (high priority): per leaf s, W_s = -Y_s T_s and the trailing update
+//       C += Y_s (W_s^T C) of every column beyond leaf s+1 (leaf s+2 waits on it);
+//   Lw (low): the panel's W (the block recurrence W_s += W_<s (Y_<s^T W_s));
+//   Lq (low): the forward Q accumulation Q(:, j0:) += (Q(:, j0:) W_k) Y_k^T per
+//       completed panel when Qf is given.
+// Every (reflector, column) pair is applied exactly once, as in Algorithm 2;
+// only the grouping of the trailing update is per leaf instead of per panel.
+// ---------------------------------------------------------------------------
+template <int M>
+bool chain_supported(int64_t Mr, int64_t K, int64_t nb) {
+  int prevB = 0;
+  for (int64_t js = 0; js < K;) {
+    const int64_t j0 = (js / nb) * nb;
+    const int B = chain_leaf_width<M>(Mr, js, j0 + nb - js);
+    if (B == 0 || (prevB && prevB != B)) return false;
+    prevB = B;
+    js += B;
+  }
+  return true;
+}
+
+template <int M>
+cudaError_t qr_factor_chain(cudaStream_t st, int64_t Mr, int64_t K, int64_t nb, Mat A, const QrBufs<M>& b, Mat Wl,
+                            Mat Tall, Mat* Qf) {
+  auto fork = [](cudaStream_t from, cudaStream_t to) {
+    cudaEvent_t ev = pool_event();
+    cudaEventRecord(ev, from);
+    cudaStreamWaitEvent(to, ev, 0);
+  };
+  cudaStream_t Lc = side_stream(0), Las = side_stream(1), Lws = side_stream(2), Lqs = side_stream(3);
+  const Lane La = b.lane(0, Las), Lw = b.lane(1, Lws), Lq = b.lane(2, Lqs);
+  fork(st, Lc);
+  fork(st, Las);
+  fork(st, Lws);
+  fork(st, Lqs);
+  if (Qf) {
+    set_stage(MDLS_ST_FORM_Q);
+    MDLS_LAUNCH(F_MISC, Lqs, set_identity_kernel<M><<<grid_for(Mr * Mr, 256), 256, 0, Lqs>>>(Mr, Mr, *Qf));
+  }
+  std::vector<int64_t> jss;
+  std::vector<int> Bs;
+  for (int64_t js = 0; js < K;) {
+    const int64_t j0 = (js / nb) * nb;
+    const int B = chain_leaf_width<M>(Mr, js, j0 + nb - js);
+    jss.push_back(js);
+    Bs.push_back(B);
+    js += B;
+  }
+  const int ns = (int)jss.size();
+  std::vector<cudaEvent_t> ev_apply((size_t)ns, nullptr);
+  for (int s = 0; s < ns; ++s) {
+    const int64_t js = jss[(size_t)s];
+    const int B = Bs[(size_t)s];
+    const int64_t j0 = (js / nb) * nb, r = Mr - js;
+    if (s >= 2) cudaStreamWaitEvent(Lc, ev_apply[(size_t)s - 2], 0);
+    set_stage(MDLS_ST_PANEL);
+    const Mat Ts{Tall.p + js * 32, 32, Tall.ps};
+    const Mat Tp = s > 0 ? Mat{Tall.p + jss[(size_t)s - 1] * 32, 32, Tall.ps} : Mat{nullptr, 0, 0};
+    cudaError_t e = launch_leaf_chain<M>(Lc, Mr, js, B, A, b.Y, b.beta, K, Ts, b.info_slot, Tp,
+                                         s > 0 ? jss[(size_t)s - 1] : -1);
+    if (e != cudaSuccess) return e;
+    cudaEvent_t ev_leaf = pool_event();
+    cudaEventRecord(ev_leaf, Lc);
+    // La: leaf W and the trailing update beyond leaf s+1
+    cudaStreamWaitEvent(Las, ev_leaf, 0);
+    const CMat Ys = sub(cm(b.Y), js, js);
+    const Mat Wls = sub(Wl, js, js);
+    set_stage(MDLS_ST_WY);
+    gemm<M, false, false>(Las, r, B, B, Ys, cm(Ts), Wls, 3, nullptr, 0);  // W_s = -Y_s T_s
+    const int64_t c0 = (s + 1 < ns) ? jss[(size_t)s + 1] + Bs[(size_t)s + 1] : K;
+    if (c0 < K) {
+      set_stage(MDLS_ST_TRAILING);
+      const Mat Cm = sub(A, js, c0);
+      gemm<M, true, false>(Las, B, K - c0, r, cm(Wls), cm(Cm), La.X, 0, La.part, La.cap);
+      gemm<M, false, false>(Las, r, K - c0, B, Ys, cm(La.X), Cm, 1, nullptr, 0);
+    }
+    ev_apply[(size_t)s] = pool_event();
+    cudaEventRecord(ev_apply[(size_t)s], Las);
+    // Lw: the panel's W, column block js..js+B-1
+    cudaStreamWaitEvent(Lws, ev_leaf, 0);
+    set_stage(MDLS_ST_WY);
+    gemm<M, false, false>(Lws, r, B, B, Ys, cm(Ts), sub(b.W, js, js), 3, nullptr, 0);
+    if (js > j0) {
+      const int64_t np = js - j0;
+      gemm<M, true, false>(Lws, np, B, r, sub(cm(b.Y), js, j0), sub(cm(b.W), js, js), Lw.X, 0, Lw.part, Lw.cap);
+      gemm<M, false, false>(Lws, Mr - j0, B, np, sub(cm(b.W), j0, j0), cm(Lw.X), sub(b.W, j0, js), 1, nullptr, 0);
+    }
+    if (Qf && (js + B == j0 + nb || s == ns - 1)) {
+      fork(Lws, Lqs);
+      const int64_t k = js / nb;
+      form_q_forward_step<M>(Lq, Mr, nb, k, *Qf, sub(cm(b.Y), j0, j0), sub(cm(b.W), j0, j0));
+    }
+  }
+  fork(Lc, st);
+  fork(Las, st);
+  fork(Lws, st);
+  fork(Lqs, st);
   return cudaGetLastError();
 }
 

@@ -60,7 +60,51 @@ void run(int Mrows, int bmax) {
   }
 }
 
+template <int M>
+void run_chain(int Mrows) {
+  using namespace mdls;
+  const int K = 32;
+  std::vector<double> h((size_t)M * Mrows * K);
+  srand(2);
+  for (size_t i = 0; i < (size_t)Mrows * K; ++i) h[i] = 2.0 * rand() / RAND_MAX - 1.0;
+  double *A, *Y, *beta, *T;
+  int* info;
+  cudaMalloc(&A, h.size() * 8);
+  cudaMalloc(&Y, h.size() * 8);
+  cudaMemset(Y, 0, h.size() * 8);
+  cudaMalloc(&beta, M * K * 8);
+  cudaMalloc(&T, M * 32 * K * 8);
+  cudaMalloc(&info, 4);
+  const int B = chain_leaf_width<M>(Mrows, 0, 16);
+  Mat Am{A, Mrows, (int64_t)Mrows * K}, Ym{Y, Mrows, (int64_t)Mrows * K};
+  for (int rep = 0; rep < 3; ++rep) {
+    cudaMemcpy(A, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
+    cudaError_t e0 = launch_leaf_chain<M>(0, Mrows, 0, B, Am, Ym, beta, K, Mat{T, 32, 32 * K}, info, Mat{nullptr, 0, 0}, -1);
+    cudaEvent_t a0, a1;
+    cudaEventCreate(&a0);
+    cudaEventCreate(&a1);
+    cudaEventRecord(a0);
+    cudaError_t e1 = launch_leaf_chain<M>(0, Mrows, B, B, Am, Ym, beta, K, Mat{T + 32 * B, 32, 32 * K}, info,
+                                          Mat{T, 32, 32 * K}, 0);
+    cudaEventRecord(a1);
+    cudaDeviceSynchronize();
+    float ms;
+    cudaEventElapsedTime(&ms, a0, a1);
+    long long p[64 * 12];
+    cudaMemcpyFromSymbol(p, g_leaf_prof, sizeof(p));
+    printf("chain M=%d rows=%d B=%d %s/%s second leaf (with prologue) %.1f us\n", M, Mrows, B, cudaGetErrorString(e0),
+           cudaGetErrorString(e1), ms * 1e3);
+    if (rep == 2) {
+      const char* names[] = {"stage", "cluster.sync", "Z partial+push", "wait Z + sum", "Z' + push", "wait Z'", "update"};
+      for (int k = 1; k <= 6; ++k) printf("  prologue %-16s %8lld cycles\n", names[k], p[63 * 12 + k] - p[63 * 12 + k - 1]);
+      printf("  prologue -> column 0 start %lld cycles\n", p[0] - p[63 * 12 + 6]);
+    }
+  }
+}
+
 int main() {
+  run_chain<2>(1024);
+  run_chain<2>(512);
   run<2>(1024, 16);
   run<2>(1024, 8);
   run<2>(512, 16);
