@@ -40,9 +40,13 @@ WORKLOADS = {
 METRIC = "md QR+backsub double-flops/s & % FP64 peak at n=1024 dd/qd/od, 1/2/4/8 B200"
 FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12      # 37.2 (FMA = 2 flops)
 FP64_PIPE_TOPS = 148 * 64 * 1.965e9 / 1e12            # 18.6 FP64-pipe lane ops/s (DADD/DMUL/DFMA each 1)
-# FP64 pipe instructions per md pair (one md mul + one md add) as the kernels implement them
-# (md.cuh Acc: dd unnormalised FMA accumulation 12; qd/od md mul + md add 182+85, 1202+269)
-OPS_PER_PAIR = {"dd": 12, "qd": 267, "od": 1471}
+# FP64 pipe instructions per md pair (one md mul + one md add) as the GEMM kernels implement them
+# (md.cuh Acc: dd unnormalised FMA pair accumulation 12; qd/od level-bin accumulation: 2M-1 FMAs +
+# sum_{n<=M-2} (n+1) [two_prod + exact deposits] = 115 / 967, + the per-k-tile bin renormalisation)
+OPS_PER_PAIR = {"dd": 12, "qd": 116, "od": 970}
+# dram traffic per launch of the roofline GEMM (1024 x 1024 x 128, C += X Y^T) from one ncu --set full
+# capture (tools/prof_gemm.py; profiles/r01_ncu_gemm_roofline.txt), bytes read + written, per precision
+GEMM_NCU_TRAFFIC = {"dd": 4294912 + 81408, "qd": 42001920 + 156672, "od": 83991040 + 14889472}
 # paper's V100 times for the same least-squares workload (T11): QR + BS kernel ms
 PAPER_V100_MS = {"dd": 451.1 + 4.0, "qd": 3020.6 + 28.0, "od": 11924.5 + 114.5}
 L2_FLUSH_BYTES = 512 << 20
@@ -138,6 +142,42 @@ def gemm_pairs(ledger):
     """md pairs computed by the md GEMM kernels (WY build, trailing update, Q formation, Q^T b)."""
     st = ledger["stages"]
     return sum(st[s]["mul"] for s in ("wy", "trailing", "form_q", "qtb"))
+
+
+def step_fp64_ops(led, prec):
+    """FP64-pipe instructions of all md pairs of the step (every stage, GEMM-rate per pair), for the GEMM share"""
+    return float(sum(v["mul"] for v in led["stages"].values())) * OPS_PER_PAIR[prec]
+
+
+def gemm_roofline(dev, prec, M, nb, reps=20, warmup=3):
+    """Roofline of the dominant kernel: the md GEMM at the solve's largest launch shape (M x M x nb,
+    C += X Y^T), timed alone with CUDA events on the current stream."""
+    import torch
+
+    import paper_2110_08375_b200 as mdls
+    from paper_2110_08375_b200 import inputs
+
+    m_l = {"dd": 2, "qd": 4, "od": 8}[prec]
+    X = torch.from_numpy(inputs.random_matrix(M, nb, prec, seed=11)).to(dev)
+    Y = torch.from_numpy(inputs.random_matrix(M, nb, prec, seed=12)).to(dev)
+    C = torch.from_numpy(inputs.random_matrix(M, M, prec, seed=13)).to(dev)
+    work = torch.empty(8 * m_l * 8 * M * M, dtype=torch.uint8, device=dev)
+    for _ in range(warmup):
+        mdls.gemm(prec, X, Y, C=C, trans_b=True, mode=1, work=work)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        mdls.gemm(prec, X, Y, C=C, trans_b=True, mode=1, work=work)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    pairs = M * M * nb
+    ops = pairs * OPS_PER_PAIR[prec]
+    achieved = ops / (ms * 1e-3) / 1e12
+    return {"ms": round(ms, 5), "ops": ops, "achieved": round(achieved, 3), "frac": round(achieved / FP64_PIPE_TOPS, 4),
+            "bytes": 8 * m_l * (2 * M * nb + 2 * M * M)}
 
 
 def run_ours(args, ws, rank, local):
@@ -268,7 +308,7 @@ def run_ours(args, ws, rank, local):
     tr = main["trace"]
     gemm_ms = tr["family_ms"]["gemm"]
     pairs = gemm_pairs(led)
-    achieved = pairs * OPS_PER_PAIR[prec] / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
+    roof = gemm_roofline(dev, prec, M, nb)
     res = {
         "metric": METRIC,
         "value": round(value, 2),
@@ -297,19 +337,26 @@ def run_ours(args, ws, rank, local):
                 "d2h_bytes_per_step": main["d2h"], "ms_per_step": round(main["e2e_ms"], 4)},
         "gpu_launches": int(main["launches_per_step"] * args.steps),
         "roofline": {
-            "kernel": "gemm_kernel (md GEMM: WY build, trailing update, Q formation, Q^T b)",
+            "kernel": "gemm_kernel (md GEMM) at the solve's largest launch: Q(:, 0:) += X Y_1^T, "
+                      f"{M} x {M} x {nb} (\"Q + QWY\", P:551-554; trailing update has the same form)",
             "bound": "alu",
-            "achieved": round(achieved, 3) if achieved else None,
+            "achieved": roof["achieved"],
             "peak": round(FP64_PIPE_TOPS, 2),
             "unit": "TFLOP/s",
-            "unit_note": "FP64-pipe lane operations (DADD/DMUL/DFMA each 1) per second; peak = 148 SMs x 64 "
-                         "lanes x 1.965 GHz (measured DADD 18.56 T/s, profiles/r01_fp64_peak.txt)",
-            "frac": round(achieved / FP64_PIPE_TOPS, 4) if achieved else None,
-            "traffic": None,
-            "algorithmic_ops_per_step": pairs * OPS_PER_PAIR[prec],
-            "kernel_ms_per_step": round(gemm_ms, 4),
-            "share_of_step": round(gemm_ms / main["ms_per_step"], 4),
-            "measured": "CUDA events around every library launch over a second traced pass of the same steps",
+            "unit_note": "FP64-pipe lane operations (DADD/DMUL/DFMA each 1) per second; algorithmic ops = md pairs x "
+                         f"{OPS_PER_PAIR[prec]} FP64 instructions per pair (md.cuh Acc); peak = 148 SMs x 64 lanes x "
+                         "1.965 GHz (measured DADD 18.56 T/s, profiles/r01_fp64_peak.txt)",
+            "frac": roof["frac"],
+            "traffic": GEMM_NCU_TRAFFIC.get(prec),
+            "algorithmic_ops_per_launch": roof["ops"],
+            "algorithmic_bytes_per_launch": roof["bytes"],
+            "launch_ms": roof["ms"],
+            "measured": "CUDA events on the launching (current torch) stream around 20 back-to-back launches "
+                        "through mdls_gemm after 3 warm-ups, inside bench.py",
+            "gemm_ops_share_of_step": round(pairs * OPS_PER_PAIR[prec] / step_fp64_ops(led, prec), 4),
+            "gemm_family_ms_traced": round(gemm_ms, 4),
+            "note": "in the solve the GEMMs run on 3 streams concurrently with the leaf chain, so traced per-launch "
+                    "times overlap; the roofline launch is timed alone",
         },
         "stages_ms": {k: round(v, 4) for k, v in tr["stages_ms"].items()},
         "family_ms": {k: round(v, 4) for k, v in tr["family_ms"].items()},

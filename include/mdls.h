@@ -140,6 +140,16 @@ int mdls_trace_collect(double *stage_ms, double *family_ms, int64_t *family_laun
   int mdls_qt_b_##P(int64_t M, int64_t N, const double *Q, int64_t ldq, int64_t psq, const double *b, int64_t psb,  \
                     double *y, int64_t psy, void *work, size_t work_bytes, void *stream);                          \
                                                                                                                    \
+  /* A3-A6 building block: the md tile product of the trailing update "YWT * C" / "R + YWTC" and    \
+   * of Q formation, C (mode)= op(A) op(B) with op(X) = X or X^T (trans_a, trans_b), op(A) m x k, op(B) k x n,       \
+   * C m x n.  mode: 0 C = P, 1 C += P, 2 C -= P, 3 C = -P.  Every product is one md mul, every sum an md add       \
+   * (dd: unnormalised pair accumulation; qd/od: level-bin accumulation); long k is split      \
+   * over CTAs and reduced in a fixed order when `work` holds >= 8*m*n*8*limbs bytes (else no split).              \
+   * All operands device, limb-planar (ptr, ld, ps); C must not alias A or B. */                                   \
+  int mdls_gemm_##P(int64_t m, int64_t n, int64_t k, int trans_a, int trans_b, const double *A, int64_t lda,       \
+                    int64_t psa, const double *B, int64_t ldb, int64_t psb, double *C, int64_t ldc, int64_t psc,   \
+                    int mode, void *work, size_t work_bytes, void *stream);                                        \
+                                                                                                                   \
   /* A7: invert the N = n/nb diagonal nb x nb tiles of the upper-triangular U (leading n x n).          \
    * Vt receives the TRANSPOSED inverses: tile i of U^-1 at columns [i*nb, (i+1)*nb) of an nb x n operand,          \
    * Vt(c, i*nb + r) = (U_i^-1)(r, c).  dev_info: first zero diagonal (1-based). */                                \

@@ -122,6 +122,29 @@ def apply_qt(prec: str, F, W, b, nb: int):
     return y
 
 
+def gemm(prec: str, A, B, C=None, trans_a: bool = False, trans_b: bool = False, mode: int = 0, work=None):
+    """md tile product C (mode)= op(A) op(B) (mdls_gemm_<p>): operands are (m, cols, rows) limb-planar tensors,
+    op(X) = X or X^T; mode 0 C = P, 1 C += P, 2 C -= P, 3 C = -P.  Returns C."""
+    torch = _torch()
+    _check_md(A, prec, 3, "A")
+    _check_md(B, prec, 3, "B")
+    m_l, ca, ra = A.shape
+    _, cb, rb = B.shape
+    m, k = (ca, ra) if trans_a else (ra, ca)
+    kb, n = (cb, rb) if trans_b else (rb, cb)
+    if kb != k:
+        raise ValueError(f"gemm: inner dimensions {k} and {kb} differ")
+    if C is None:
+        C = torch.zeros((m_l, n, m), dtype=torch.float64, device=A.device)
+    _check_md(C, prec, 3, "C")
+    if work is None:
+        work = torch.empty(8 * m_l * 8 * max(m * n, 1), dtype=torch.uint8, device=A.device)
+    rc = _lib.fn("mdls_gemm_", prec)(m, n, k, int(trans_a), int(trans_b), *_mat(A), *_mat(B), *_mat(C), mode,
+                                     _ptr(work), work.numel(), _stream())
+    _lib.check(rc, "gemm")
+    return C
+
+
 def qt_b(prec: str, Q, b):
     """y = Q^T b with an explicit Q of shape (m, N, M) (N columns of M rows); y has N entries."""
     torch = _torch()

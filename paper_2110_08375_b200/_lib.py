@@ -43,6 +43,7 @@ _SIGS = {
     "mdls_qr_": (_I, [_L, _L, _L, _P, _L, _L, _P, _L, _L, _P, _L, _L, _P, _Z, _P, _P]),
     "mdls_apply_qt_": (_I, [_L, _L, _L, _P, _L, _L, _P, _L, _L, _P, _L, _P, _L, _P, _Z, _P]),
     "mdls_qt_b_": (_I, [_L, _L, _P, _L, _L, _P, _L, _P, _L, _P, _Z, _P]),
+    "mdls_gemm_": (_I, [_L, _L, _L, _I, _I, _P, _L, _L, _P, _L, _L, _P, _L, _L, _I, _P, _Z, _P]),
     "mdls_invert_tiles_": (_I, [_L, _L, _P, _L, _L, _P, _L, _L, _P, _P]),
     "mdls_backsub_": (_I, [_L, _L, _P, _L, _L, _P, _L, _P, _L, _P, _Z, _P, _P]),
     "mdls_lstsq_": (_I, [_L, _L, _L, _P, _L, _L, _P, _L, _P, _L, _I, _P, _L, _L, _P, _L, _L, _P, _L, _P, _Z, _P,

@@ -227,6 +227,38 @@ int MDLS_FN(mdls_qt_b_)(int64_t Mr, int64_t Nc, const double* Q, int64_t ldq, in
   return launched();
 }
 
+int MDLS_FN(mdls_gemm_)(int64_t m, int64_t n, int64_t k, int trans_a, int trans_b, const double* A, int64_t lda,
+                        int64_t psa, const double* B, int64_t ldb, int64_t psb, double* C, int64_t ldc, int64_t psc,
+                        int mode, void* work, size_t work_bytes, void* stream) {
+  if (m < 0) return -1;
+  if (n < 0) return -2;
+  if (k < 0) return -3;
+  if (trans_a < 0 || trans_a > 1) return -4;
+  if (trans_b < 0 || trans_b > 1) return -5;
+  if (m == 0 || n == 0) return 0;
+  if (!mat_ok(A, trans_a ? k : m, trans_a ? m : k, lda, psa)) return -6;
+  if (!mat_ok(B, trans_b ? n : k, trans_b ? k : n, ldb, psb)) return -9;
+  if (!mat_ok(C, m, n, ldc, psc) || C == A || C == B) return -12;
+  if (mode < 0 || mode > 3) return -15;
+  cudaStream_t st = S(stream);
+  set_stage(MDLS_NSTAGES);
+  const size_t need = sizeof(double) * M * kMaxSplit * m * n;
+  double* part = (work && work_bytes >= need) ? static_cast<double*>(work) : nullptr;
+  const int64_t cap = part ? kMaxSplit * m * n : 0;
+  const CMat Am{A, lda, psa}, Bm{B, ldb, psb};
+  const Mat Cm{C, ldc, psc};
+  if (k == 0) {
+    if (mode == 0 || mode == 3)
+      MDLS_LAUNCH(F_MISC, st, set_zero_kernel<M><<<grid_for(m * n, 256), 256, 0, st>>>(m, n, Cm));
+    return launched();
+  }
+  if (trans_a && trans_b) gemm<M, true, true>(st, m, n, k, Am, Bm, Cm, mode, part, cap);
+  else if (trans_a) gemm<M, true, false>(st, m, n, k, Am, Bm, Cm, mode, part, cap);
+  else if (trans_b) gemm<M, false, true>(st, m, n, k, Am, Bm, Cm, mode, part, cap);
+  else gemm<M, false, false>(st, m, n, k, Am, Bm, Cm, mode, part, cap);
+  return launched();
+}
+
 int MDLS_FN(mdls_lstsq_)(int64_t Mr, int64_t K, int64_t nb, const double* A, int64_t lda, int64_t psa,
                          const double* b, int64_t psb, double* x, int64_t psx, int form_q, double* R_out, int64_t ldr,
                          int64_t psr, double* Q_out, int64_t ldq, int64_t psq, double* y_out, int64_t psy, void* work,

@@ -4,4 +4,5 @@ namespace mdls {
 MDLS_INSTANTIATE_GEMM(8, true, false)
 MDLS_INSTANTIATE_GEMM(8, false, true)
 MDLS_INSTANTIATE_GEMM(8, false, false)
+MDLS_INSTANTIATE_GEMM(8, true, true)
 }  // namespace mdls

@@ -4,4 +4,5 @@ namespace mdls {
 MDLS_INSTANTIATE_GEMM(4, true, false)
 MDLS_INSTANTIATE_GEMM(4, false, true)
 MDLS_INSTANTIATE_GEMM(4, false, false)
+MDLS_INSTANTIATE_GEMM(4, true, true)
 }  // namespace mdls

@@ -69,6 +69,17 @@ __global__ void set_identity_kernel(int64_t rows, int64_t cols, Mat q) {
   }
 }
 
+// C = 0 on rows x cols
+template <int M>
+__global__ void set_zero_kernel(int64_t rows, int64_t cols, Mat q) {
+  const int64_t total = rows * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % rows, j = e / rows;
+#pragma unroll
+    for (int k = 0; k < M; ++k) q.p[k * q.ps + j * q.ld + i] = 0.0;
+  }
+}
+
 // info <- -1 if any limb of the rows x cols operand is not finite
 template <int M>
 __global__ void finite_check_kernel(int64_t rows, int64_t cols, CMat a, int* info) {
