@@ -35,12 +35,27 @@ def _nvcc() -> str:
     return cand
 
 
+def _deps(path: str, seen: set | None = None) -> set:
+    """the file and every quoted #include it reaches (recursively)"""
+    seen = set() if seen is None else seen
+    path = os.path.normpath(path)
+    if path in seen or not os.path.exists(path):
+        return seen
+    seen.add(path)
+    with open(path) as f:
+        for line in f:
+            line = line.strip()
+            if line.startswith("#include \""):
+                inc = line.split('"')[1]
+                _deps(os.path.join(os.path.dirname(path), inc), seen)
+    return seen
+
+
 def _stale(obj: str, src: str) -> bool:
     if not os.path.exists(obj):
         return True
     t = os.path.getmtime(obj)
-    deps = [src] + [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(HERE, "..", "include", "mdls.h")]
-    return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
+    return any(os.path.getmtime(d) > t for d in _deps(src))
 
 
 def build(force: bool = False, verbose: bool = False, extra: list[str] | None = None) -> str:

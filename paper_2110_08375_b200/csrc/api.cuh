@@ -176,7 +176,8 @@ int MDLS_FN(mdls_qr_)(int64_t Mr, int64_t K, int64_t nb, double* A, int64_t lda,
   const bool fwd = Q && q_forward<M>();
   if (use_chain<M>(Mr, K, nb)) {
     if (qr_factor_chain<M>(st, Mr, K, nb, Am, b, Mat{at<double>(work, p.wl), Mr, Mr * K},
-                           Mat{at<double>(work, p.t), 32, 32 * std::max<int64_t>(K, 32)}, fwd ? &Qm : nullptr) != cudaSuccess)
+                           Mat{at<double>(work, p.t), 32, 32 * std::max<int64_t>(K, 32)}, fwd ? &Qm : nullptr,
+                           at<int>(work, p.flags)) != cudaSuccess)
       return MDLS_ERR_CUDA;
   } else if (qr_factor_overlap<M>(b.lane(0, st), b.lane(1, side_stream(0)), b.lane(2, side_stream(1)), Mr, K, nb, Am,
                                   b, fwd ? &Qm : nullptr) != cudaSuccess) {
@@ -292,7 +293,8 @@ int MDLS_FN(mdls_lstsq_)(int64_t Mr, int64_t K, int64_t nb, const double* A, int
   const bool fwd = form_q && q_forward<M>();
   if (use_chain<M>(Mr, K, nb)) {
     if (qr_factor_chain<M>(st, Mr, K, nb, Af, bb, Mat{at<double>(work, p.wl), Mr, Mr * K},
-                           Mat{at<double>(work, p.t), 32, 32 * std::max<int64_t>(K, 32)}, fwd ? &Q : nullptr) != cudaSuccess)
+                           Mat{at<double>(work, p.t), 32, 32 * std::max<int64_t>(K, 32)}, fwd ? &Q : nullptr,
+                           at<int>(work, p.flags)) != cudaSuccess)
       return MDLS_ERR_CUDA;
   } else if (qr_factor_overlap<M>(bb.lane(0, st), bb.lane(1, side_stream(0)), bb.lane(2, side_stream(1)), Mr, K, nb,
                                   Af, bb, fwd ? &Q : nullptr) != cudaSuccess) {

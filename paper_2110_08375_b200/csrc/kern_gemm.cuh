@@ -118,8 +118,19 @@ __global__ void splitk_reduce_kernel(int64_t m, int64_t n, int64_t S, const doub
   const int64_t total = m * n, pps = m * n * S;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = e % m, j = e / m;
-    md<M> s = ld<M>(part, pps, e);
-    for (int64_t z = 1; z < S; ++z) s = add<M>(s, ld<M>(part, pps, i + (j + z * n) * m));
+    // exact merges of the split partials (md.cuh Acc: bins = limbs), one normalisation
+    Acc<M> acc;
+    const md<M> p0 = ld<M>(part, pps, e);
+#pragma unroll
+    for (int k = 0; k < Acc<M>::NV; ++k) acc.r(k) = (k < M) ? p0.v[k] : 0.0;
+    for (int64_t z = 1; z < S; ++z) {
+      const md<M> pz = ld<M>(part, pps, i + (j + z * n) * m);
+      Acc<M> o;
+#pragma unroll
+      for (int k = 0; k < Acc<M>::NV; ++k) o.r(k) = (k < M) ? pz.v[k] : 0.0;
+      acc.merge(o);
+    }
+    const md<M> s = acc.get();
     const int64_t ce = i + j * ldc;
     md<M> c = (mode == 1 || mode == 2) ? ld<M>(C, psc, ce) : md_zero<M>();
     st<M>(C, psc, ce, apply_mode<M>(mode, c, s));
@@ -166,12 +177,28 @@ void gemm(cudaStream_t st, int64_t m, int64_t n, int64_t k, CMat A, CMat B, Mat 
   } else {
     const int64_t t0 = cdiv(m, GemmTile<M, 0>::BM) * cdiv(n, GemmTile<M, 0>::BN);
     const bool can_split = part && k >= 8 * GemmTile<M, 0>::BK;
-    if (t0 >= target || (can_split && t0 >= target / 8)) gemm_launch<M, 0, TA, TB>(st, m, n, k, A, B, C, mode, part, part_cap_elems);
+    // the large tile once it fills about a wave (2 CTAs per SM resident), or with split-K
+    if (t0 >= (2 * kNumSMs) / 3 || (can_split && t0 >= target / 8))
+      gemm_launch<M, 0, TA, TB>(st, m, n, k, A, B, C, mode, part, part_cap_elems);
     else gemm_launch<M, 1, TA, TB>(st, m, n, k, A, B, C, mode, part, part_cap_elems);
   }
 }
 
+// Load every md GEMM kernel of this precision/transposition now.  With CUDA's lazy module
+// loading, a kernel's first launch loads it, which must not happen while the persistent leaf
+// chain (solver.cuh::qr_factor_chain) waits for work on other streams.
+template <int M, bool TA, bool TB>
+void gemm_preload() {
+  cudaFuncAttributes fa{};
+  cudaFuncGetAttributes(&fa, gemm_kernel<M, 0, TA, TB>);
+  cudaFuncGetAttributes(&fa, gemm_kernel<M, 1, TA, TB>);
+  cudaFuncGetAttributes(&fa, gemm_kernel<M, 2, TA, TB>);
+  cudaFuncGetAttributes(&fa, gemm_kernel<M, 3, TA, TB>);
+  cudaFuncGetAttributes(&fa, splitk_reduce_kernel<M>);
+}
+
 #define MDLS_INSTANTIATE_GEMM(MM, TA, TB)                                                                   \
-  template void gemm<MM, TA, TB>(cudaStream_t, int64_t, int64_t, int64_t, CMat, CMat, Mat, int, double*, int64_t);
+  template void gemm<MM, TA, TB>(cudaStream_t, int64_t, int64_t, int64_t, CMat, CMat, Mat, int, double*, int64_t); \
+  template void gemm_preload<MM, TA, TB>();
 
 }  // namespace mdls

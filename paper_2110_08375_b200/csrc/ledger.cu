@@ -100,6 +100,36 @@ void trace_end(cudaStream_t st, int family) {
   g_recs.push_back(Rec{t_stage, family, t_open, e1});
   t_open = nullptr;
 }
+// flags between the persistent leaf chain and the streams around it (solver.cuh::qr_factor_chain)
+__global__ void wait_flag_kernel(const int* f) {
+  if (threadIdx.x == 0) {
+    int v = 0;
+    do {
+      asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+      if (v == 0) __nanosleep(256);
+    } while (v == 0);
+  }
+}
+__global__ void set_flag_kernel(int* f) {
+  __threadfence();
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" :: "l"(f), "r"(1) : "memory");
+}
+void launch_wait_flag(cudaStream_t st, const int* f) {
+  trace_begin(st, 4 /* F_MISC */);
+  wait_flag_kernel<<<1, 32, 0, st>>>(f);
+  trace_end(st, 4 /* F_MISC */);
+}
+void flags_preload() {
+  cudaFuncAttributes fa{};
+  cudaFuncGetAttributes(&fa, wait_flag_kernel);
+  cudaFuncGetAttributes(&fa, set_flag_kernel);
+}
+void launch_set_flag(cudaStream_t st, int* f) {
+  trace_begin(st, 4 /* F_MISC */);
+  set_flag_kernel<<<1, 1, 0, st>>>(f);
+  trace_end(st, 4 /* F_MISC */);
+}
+
 }  // namespace mdls
 
 namespace {

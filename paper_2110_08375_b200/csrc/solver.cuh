@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdint>
 #include <cstring>
 #include <vector>
@@ -22,7 +23,7 @@ namespace mdls {
 // workspace plan (bytes, 256-aligned segments)
 // ---------------------------------------------------------------------------
 struct Plan {
-  size_t af = 0, q = 0, y = 0, w = 0, wl = 0, beta = 0, s = 0, t = 0, x = 0, part = 0, v0 = 0, v1 = 0, v2 = 0, vt = 0,
+  size_t af = 0, q = 0, y = 0, w = 0, wl = 0, flags = 0, beta = 0, s = 0, t = 0, x = 0, part = 0, v0 = 0, v1 = 0, v2 = 0, vt = 0,
          info = 0, total = 0;
 };
 
@@ -47,11 +48,12 @@ Plan make_plan(int op, int64_t Mr, int64_t K, int64_t nb) {
     p.s = take(md * nb * nb);
     p.t = take(md * std::max<int64_t>(std::max<int64_t>(nb * nb, 1024), 32 * K));  // leaf T's (ld 32, column js)
     p.wl = take(md * Mr * K);                                                       // leaf-local W_s = -Y_s T_s
+    p.flags = take(2 * sizeof(int) * (size_t)K);                                    // persistent-chain flags
   }
   if (op == MDLS_OP_APPLY_QT) p.y = take(md * Mr * K);
   if (qr_like || op == MDLS_OP_APPLY_QT) {
-    p.x = take(3 * md * nb * mx);  // one GEMM-intermediate buffer per stream lane
-    p.part = take(3 * md * kMaxSplit * nb * mx);
+    p.x = take(4 * md * nb * mx);  // one GEMM-intermediate buffer per stream lane
+    p.part = take(4 * md * kMaxSplit * nb * mx);
   }
   p.v0 = take(md * mx);
   p.v1 = take(md * mx);
@@ -236,7 +238,20 @@ bool chain_supported(int64_t Mr, int64_t K, int64_t nb) {
 
 template <int M>
 cudaError_t qr_factor_chain(cudaStream_t st, int64_t Mr, int64_t K, int64_t nb, Mat A, const QrBufs<M>& b, Mat Wl,
-                            Mat Tall, Mat* Qf) {
+                            Mat Tall, Mat* Qf, int* flags) {
+  // MDLS_PERSIST=1: persistent leaf chain (one cluster launch for all leaves, flags between the
+  // streams).  Off by default: it relies on concurrent kernel execution (it deadlocks when kernels
+  // are serialised, e.g. under a profiler's replay or CUDA_LAUNCH_BLOCKING=1).
+  // The previous-leaf prologue (in-cluster) applies leaf s-1 to leaf s's columns; MDLS_PROLOGUE=0
+  // applies it with GEMMs between the leaves instead (on the chain stream).
+  static const bool pro = [] {
+    const char* v = getenv("MDLS_PROLOGUE");
+    return v ? v[0] == '1' : true;  // measured: the GEMM variant is slower for qd/od too (39.8 vs 33.6 ms qd)
+  }();
+  static const bool persist = [] {
+    const char* v = getenv("MDLS_PERSIST");
+    return v && v[0] == '1';
+  }() && pro;
   auto fork = [](cudaStream_t from, cudaStream_t to) {
     cudaEvent_t ev = pool_event();
     cudaEventRecord(ev, from);
@@ -244,6 +259,19 @@ cudaError_t qr_factor_chain(cudaStream_t st, int64_t Mr, int64_t K, int64_t nb, 
   };
   cudaStream_t Lc = side_stream(0), Las = side_stream(1), Lws = side_stream(2), Lqs = side_stream(3);
   const Lane La = b.lane(0, Las), Lw = b.lane(1, Lws), Lq = b.lane(2, Lqs);
+  if (persist) {
+    static bool loaded = false;  // lazy module loading must not happen while the chain spins
+    if (!loaded) {
+      gemm_preload<M, false, false>();
+      gemm_preload<M, true, false>();
+      gemm_preload<M, false, true>();
+      flags_preload();
+      cudaFuncAttributes fa{};
+      cudaFuncGetAttributes(&fa, set_identity_kernel<M>);
+      loaded = true;
+    }
+    cudaMemsetAsync(flags, 0, 2 * sizeof(int) * (size_t)K, st);
+  }
   fork(st, Lc);
   fork(st, Las);
   fork(st, Lws);
@@ -262,35 +290,92 @@ cudaError_t qr_factor_chain(cudaStream_t st, int64_t Mr, int64_t K, int64_t nb, 
     js += B;
   }
   const int ns = (int)jss.size();
+  int* leaf_done = flags;
+  int* apply_done = flags + ns;
+  if (persist) {
+    set_stage(MDLS_ST_PANEL);
+    cudaError_t e = launch_leaf_persistent<M>(Lc, Mr, ns, Bs[0], A, b.Y, b.beta, K, Tall, b.info_slot, leaf_done,
+                                              apply_done);
+    if (e != cudaSuccess) return e;
+  }
   std::vector<cudaEvent_t> ev_apply((size_t)ns, nullptr);
+  // MDLS_TIMELINE=1 (debug, not graph-capturable): per-leaf start/end and apply-end times, printed
+  static const bool timeline = getenv("MDLS_TIMELINE") != nullptr;
+  std::vector<cudaEvent_t> tl_ls, tl_le, tl_ae;
+  cudaEvent_t tl0 = nullptr;
+  auto tl_ev = [](cudaStream_t q) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, q);
+    return e;
+  };
+  if (timeline) tl0 = tl_ev(Lc);
   for (int s = 0; s < ns; ++s) {
     const int64_t js = jss[(size_t)s];
     const int B = Bs[(size_t)s];
     const int64_t j0 = (js / nb) * nb, r = Mr - js;
-    if (s >= 2) cudaStreamWaitEvent(Lc, ev_apply[(size_t)s - 2], 0);
-    set_stage(MDLS_ST_PANEL);
     const Mat Ts{Tall.p + js * 32, 32, Tall.ps};
-    const Mat Tp = s > 0 ? Mat{Tall.p + jss[(size_t)s - 1] * 32, 32, Tall.ps} : Mat{nullptr, 0, 0};
-    cudaError_t e = launch_leaf_chain<M>(Lc, Mr, js, B, A, b.Y, b.beta, K, Ts, b.info_slot, Tp,
-                                         s > 0 ? jss[(size_t)s - 1] : -1);
-    if (e != cudaSuccess) return e;
     cudaEvent_t ev_leaf = pool_event();
-    cudaEventRecord(ev_leaf, Lc);
+    if (persist) {
+      set_stage(MDLS_ST_PANEL);
+      launch_wait_flag(Las, leaf_done + s);
+      cudaEventRecord(ev_leaf, Las);
+    } else {
+      if (s >= 2) cudaStreamWaitEvent(Lc, ev_apply[(size_t)s - 2], 0);
+      if (timeline) tl_ls.push_back(tl_ev(Lc));
+      set_stage(MDLS_ST_PANEL);
+      const Mat Tp = s > 0 ? Mat{Tall.p + jss[(size_t)s - 1] * 32, 32, Tall.ps} : Mat{nullptr, 0, 0};
+      cudaError_t e = launch_leaf_chain<M>(Lc, Mr, js, B, A, b.Y, b.beta, K, Ts, b.info_slot, Tp,
+                                           (pro && s > 0) ? jss[(size_t)s - 1] : -1);
+      if (e != cudaSuccess) return e;
+      if (!pro) {  // W_s = -Y_s T_s and leaf s applied to leaf s+1's columns, on the chain
+        const Lane Lcl = b.lane(3, Lc);
+        set_stage(MDLS_ST_WY);
+        gemm<M, false, false>(Lc, r, B, B, sub(cm(b.Y), js, js), cm(Ts), sub(Wl, js, js), 3, nullptr, 0);
+        if (s + 1 < ns) {
+          set_stage(MDLS_ST_PANEL);
+          // leaf s+1's columns must have leaf s-1 applied (La) before leaf s is applied here
+          if (s >= 1) cudaStreamWaitEvent(Lc, ev_apply[(size_t)s - 1], 0);
+          const int64_t jn = jss[(size_t)s + 1];
+          const int Bn = Bs[(size_t)s + 1];
+          const Mat Cn = sub(A, js, jn);
+          gemm<M, true, false>(Lc, B, Bn, r, sub(cm(Wl), js, js), cm(Cn), Lcl.X, 0, Lcl.part, Lcl.cap);
+          gemm<M, false, false>(Lc, r, Bn, B, sub(cm(b.Y), js, js), cm(Lcl.X), Cn, 1, nullptr, 0);
+        }
+      }
+      cudaEventRecord(ev_leaf, Lc);
+      if (timeline) tl_le.push_back(tl_ev(Lc));
+    }
     // La: leaf W and the trailing update beyond leaf s+1
     cudaStreamWaitEvent(Las, ev_leaf, 0);
     const CMat Ys = sub(cm(b.Y), js, js);
     const Mat Wls = sub(Wl, js, js);
-    set_stage(MDLS_ST_WY);
-    gemm<M, false, false>(Las, r, B, B, Ys, cm(Ts), Wls, 3, nullptr, 0);  // W_s = -Y_s T_s
     const int64_t c0 = (s + 1 < ns) ? jss[(size_t)s + 1] + Bs[(size_t)s + 1] : K;
-    if (c0 < K) {
+    // dd: the whole trailing update of leaf s as one cluster launch (leaf_apply_kernel); else GEMMs
+    static const bool fused = [] {  // measured slower than the GEMMs (5.27 vs 4.97 ms dd without Q): opt-in
+      const char* v = getenv("MDLS_FUSED_APPLY");
+      return v && v[0] == '1';
+    }();
+    bool done = false;
+    if (fused && pro && c0 < K) {
       set_stage(MDLS_ST_TRAILING);
-      const Mat Cm = sub(A, js, c0);
-      gemm<M, true, false>(Las, B, K - c0, r, cm(Wls), cm(Cm), La.X, 0, La.part, La.cap);
-      gemm<M, false, false>(Las, r, K - c0, B, Ys, cm(La.X), Cm, 1, nullptr, 0);
+      done = launch_leaf_apply<M>(Las, Mr, js, B, A, b.Y, Ts, c0, K) == cudaSuccess;
+      if (!done) cudaGetLastError();
     }
+    if (!done) {
+      set_stage(MDLS_ST_WY);
+      if (pro) gemm<M, false, false>(Las, r, B, B, Ys, cm(Ts), Wls, 3, nullptr, 0);  // W_s = -Y_s T_s
+      if (c0 < K) {
+        set_stage(MDLS_ST_TRAILING);
+        const Mat Cm = sub(A, js, c0);
+        gemm<M, true, false>(Las, B, K - c0, r, cm(Wls), cm(Cm), La.X, 0, La.part, La.cap);
+        gemm<M, false, false>(Las, r, K - c0, B, Ys, cm(La.X), Cm, 1, nullptr, 0);
+      }
+    }
+    if (persist) launch_set_flag(Las, apply_done + s);
     ev_apply[(size_t)s] = pool_event();
     cudaEventRecord(ev_apply[(size_t)s], Las);
+    if (timeline) tl_ae.push_back(tl_ev(Las));
     // Lw: the panel's W, column block js..js+B-1
     cudaStreamWaitEvent(Lws, ev_leaf, 0);
     set_stage(MDLS_ST_WY);
@@ -310,6 +395,23 @@ cudaError_t qr_factor_chain(cudaStream_t st, int64_t Mr, int64_t K, int64_t nb, 
   fork(Las, st);
   fork(Lws, st);
   fork(Lqs, st);
+  if (timeline) {
+    cudaEvent_t tw = tl_ev(Lws), tq = tl_ev(Lqs);
+    cudaDeviceSynchronize();
+    float t;
+    for (size_t s = 0; s < tl_ae.size(); ++s) {
+      float a0 = 0, a1 = 0, a2 = 0;
+      if (s < tl_ls.size()) cudaEventElapsedTime(&a0, tl0, tl_ls[s]);
+      if (s < tl_le.size()) cudaEventElapsedTime(&a1, tl0, tl_le[s]);
+      cudaEventElapsedTime(&a2, tl0, tl_ae[s]);
+      printf("leaf %3zu start %8.1f end %8.1f (%6.1f us)  apply end %8.1f us\n", s, a0 * 1e3, a1 * 1e3,
+             (a1 - a0) * 1e3, a2 * 1e3);
+    }
+    cudaEventElapsedTime(&t, tl0, tw);
+    printf("W stream end %8.1f us\n", t * 1e3);
+    cudaEventElapsedTime(&t, tl0, tq);
+    printf("Q stream end %8.1f us\n", t * 1e3);
+  }
   return cudaGetLastError();
 }
 
