@@ -684,6 +684,24 @@ __device__ __forceinline__ void leaf_prologue(const LeafArgs<M>& a, cg::cluster_
   (void)lane;
 }
 
+// Column ll of the leaf's compact-WY T for the rows r = rank (mod C):
+//   T(ll, ll) = beta_ll,  T(r, ll) = -beta_ll sum_{p=r}^{ll-1} T(r, p) Y_p^T v_ll   (W = -Y T)
+// one lane per row, the <= B-1 terms accumulated in a level-bin / pair accumulator (no warp tree).
+template <int M, int BT>
+__device__ __forceinline__ void leaf_t_column(md<M> (&Ts)[BT][BT], const md<M> (&SY)[BT][BT], const md<M> (&betas)[BT],
+                                              int ll, int rank, int C, int lane) {
+  const int r = rank + lane * C;
+  if (r > ll) return;
+  if (r == ll) {
+    Ts[ll][ll] = betas[ll];
+    return;
+  }
+  Acc<M> acc;
+  acc.init();
+  for (int p = r; p < ll; ++p) acc.add_prod(Ts[r][p], SY[p][ll]);
+  Ts[r][ll] = neg(mul<M>(betas[ll], acc.get()));
+}
+
 // One leaf (the body of leaf_reg_kernel; leaf_chain_kernel runs it for every leaf of the
 // factorisation).  init_bars: initialise the column mbarriers (first leaf of the kernel);
 // zinit / zpar: initialise the prologue mbarriers / their phase parity for this leaf.
@@ -866,18 +884,7 @@ __device__ __forceinline__ void leaf_body(const LeafArgs<M>& a, bool init_bars, 
         sc_mu = x1;
       }
     }
-    if (warp == 3 && l > 0) {  // extend this CTA's rows of the leaf T by column l-1
-      const int ll = l - 1;
-      for (int r = rank; r <= ll; r += C) {
-        if (r == ll) {
-          if (lane == 0) Ts[ll][ll] = betas[ll];
-          continue;
-        }
-        md<M> s = (lane >= r && lane < ll) ? mul<M>(Ts[r][lane], SY[lane][ll]) : md_zero<M>();
-        s = warp_sum<M>(s);
-        if (lane == 0) Ts[r][ll] = neg(mul<M>(betas[ll], s));
-      }
-    }
+    if (warp == 3 && l > 0) leaf_t_column<M>(Ts, SY, betas, l - 1, rank, C, lane);  // this CTA's rows of T(:, l-1)
     __syncthreads();
     LEAF_MARK(l, 5);
     if constexpr (M != 2) {
@@ -932,18 +939,7 @@ __device__ __forceinline__ void leaf_body(const LeafArgs<M>& a, bool init_bars, 
 
   // ---- last T column, write-back of R/v, explicit Y, beta, T ----
   __syncthreads();
-  if (warp == 3) {
-    const int ll = B - 1;
-    for (int r = rank; r <= ll; r += C) {
-      if (r == ll) {
-        if (lane == 0) Ts[ll][ll] = betas[ll];
-        continue;
-      }
-      md<M> s = (lane >= r && lane < ll) ? mul<M>(Ts[r][lane], SY[lane][ll]) : md_zero<M>();
-      s = warp_sum<M>(s);
-      if (lane == 0) Ts[r][ll] = neg(mul<M>(betas[ll], s));
-    }
-  }
+  if (warp == 3) leaf_t_column<M>(Ts, SY, betas, B - 1, rank, C, lane);
   if (valid) {
 #pragma unroll
     for (int q = 0; q < V; ++q) {

@@ -103,6 +103,13 @@ void run_chain(int Mrows) {
 }
 
 int main() {
+#ifdef PROF_OD
+  run_chain<8>(1024);
+  run<8>(1024, 8);
+  run_chain<4>(1024);
+  run<4>(1024, 8);
+  return 0;
+#endif
   run_chain<2>(1024);
   run_chain<2>(512);
   run<2>(1024, 16);
