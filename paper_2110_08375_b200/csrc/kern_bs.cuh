@@ -85,8 +85,10 @@ __global__ void __launch_bounds__(256) bs_mulinv_kernel(int64_t nb, int64_t tile
     md<M> bb = ld<M>(b, psb, base + c);
     acc.add_prod(t, bb);
   }
-  md<M> s = warp_sum<M>(acc.get());
-  if (lane == 0) st<M>(x, psx, base + r, s);
+  // fixed-order tree of exact accumulator merges (no renormalised md add per level)
+#pragma unroll
+  for (int d = 16; d >= 1; d >>= 1) acc.merge(acc_shfl_down<M>(acc, d));
+  if (lane == 0) st<M>(x, psx, base + r, acc.get());
 }
 
 // ============================================================================
@@ -98,7 +100,7 @@ __global__ void __launch_bounds__(256) bs_mulinv_kernel(int64_t nb, int64_t tile
 template <int M, int G, int RPT>
 __global__ void __launch_bounds__(32 * G) bs_update_kernel(int64_t nb, int64_t tile, int64_t row0, int64_t row1, CMat U,
                                                            const double* x, int64_t psx, double* b, int64_t psb) {
-  __shared__ md<M> part[G][32 * RPT];
+  __shared__ Acc<M> part[G][32 * RPT];
   const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
   const int64_t rbase = row0 + (int64_t)blockIdx.x * 32 * RPT;
   const int64_t base = tile * nb;
@@ -114,14 +116,25 @@ __global__ void __launch_bounds__(32 * G) bs_update_kernel(int64_t nb, int64_t t
     }
   }
 #pragma unroll
-  for (int t = 0; t < RPT; ++t) part[g][lane + 32 * t] = acc[t].get();
+  for (int t = 0; t < RPT; ++t) part[g][lane + 32 * t] = acc[t];
   __syncthreads();
+  // fixed-order tree over the G column groups (exact accumulator merges)
+#pragma unroll
+  for (int stride = G / 2; stride >= 1; stride >>= 1) {
+    if (g < stride) {
+#pragma unroll
+      for (int t = 0; t < RPT; ++t) {
+        Acc<M> a = part[g][lane + 32 * t];
+        a.merge(part[g + stride][lane + 32 * t]);
+        part[g][lane + 32 * t] = a;
+      }
+    }
+    __syncthreads();
+  }
   for (int e = threadIdx.x; e < 32 * RPT; e += 32 * G) {
     const int64_t rho = rbase + e;
     if (rho >= row1) continue;
-    md<M> t = part[0][e];
-#pragma unroll
-    for (int q = 1; q < G; ++q) t = add<M>(t, part[q][e]);
+    const md<M> t = part[0][e].get();
     md<M> bb = ld<M>(b, psb, rho);
     st<M>(b, psb, rho, add<M>(bb, neg(t)));
   }

@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <cstring>
 #include <vector>
@@ -476,7 +477,11 @@ void backsub(cudaStream_t st, int64_t n, int64_t nb, CMat U, const double* y, in
   };
   fork(st, sinv);
   set_stage(MDLS_ST_INVERT);
-  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(N, 16));
+  static const int64_t chunk_env = [] {
+    const char* v = getenv("MDLS_INV_CHUNK");
+    return (int64_t)(v ? atoi(v) : 16);
+  }();
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(N, chunk_env > 0 ? chunk_env : N));
   std::vector<cudaEvent_t> inv_ready((size_t)N, nullptr);
   for (int64_t hi = N; hi > 0; hi -= chunk) {
     const int64_t lo = std::max<int64_t>(0, hi - chunk);
