@@ -36,15 +36,22 @@ __global__ void __launch_bounds__(256) invert_tiles_kernel(int64_t nb, CMat U, M
 
   for (int64_t k = (int64_t)blockIdx.y * nwarp + warp; k < nb; k += (int64_t)gridDim.y * nwarp) {
     const bool degk = dbeta && dbeta[k] == 0.0;
-    md<M> s[NPL];
+    // row accumulators s_i = e_k(i) - sum_l u_il x_l (md.cuh Acc: exact deposits, normalised only
+    // when row i becomes the pivot row l)
+    Acc<M> s[NPL];
 #pragma unroll
-    for (int t = 0; t < NPL; ++t) s[t] = md_from<M>((lane + 32 * t == k) ? 1.0 : 0.0);
+    for (int t = 0; t < NPL; ++t) {
+      s[t].init();
+      if (lane + 32 * t == k) s[t].r(0) = 1.0;
+    }
     for (int64_t l = k; l >= 0; --l) {
       const int ol = (int)(l & 31), tl = (int)(l >> 5);
-      md<M> sl = s[0];
+      Acc<M> sa = s[0];
 #pragma unroll
       for (int t = 1; t < NPL; ++t)
-        if (t == tl) sl = s[t];
+#pragma unroll
+        for (int q = 0; q < Acc<M>::NV; ++q) sa.r(q) = (t == tl) ? s[t].r(q) : sa.r(q);
+      const md<M> sl = sa.get();
       md<M> rinv;
 #pragma unroll
       for (int q = 0; q < M; ++q) rinv.v[q] = smem_inv[q * nb + l];
@@ -59,7 +66,7 @@ __global__ void __launch_bounds__(256) invert_tiles_kernel(int64_t nb, CMat U, M
         if (i < l) {
           md<M> u = (degl || (dbeta && dbeta[i] == 0.0)) ? md_zero<M>()
                                                            : ld<M>(U.p, U.ps, (base + i) + (base + l) * U.ld);
-          s[t] = fma<M>(s[t], u, nx);
+          s[t].add_prod(u, nx);
         }
       }
     }

@@ -479,7 +479,7 @@ void backsub(cudaStream_t st, int64_t n, int64_t nb, CMat U, const double* y, in
   set_stage(MDLS_ST_INVERT);
   static const int64_t chunk_env = [] {
     const char* v = getenv("MDLS_INV_CHUNK");
-    return (int64_t)(v ? atoi(v) : 16);
+    return (int64_t)(v ? atoi(v) : 0);  // 0: all tiles in one launch (measured 5.41 vs 5.50 ms at n = 17920)
   }();
   const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(N, chunk_env > 0 ? chunk_env : N));
   std::vector<cudaEvent_t> inv_ready((size_t)N, nullptr);
