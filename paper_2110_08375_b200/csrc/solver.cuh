@@ -252,7 +252,7 @@ cudaError_t qr_factor_chain(cudaStream_t st, int64_t Mr, int64_t K, int64_t nb, 
   static const bool persist = [] {
     const char* v = getenv("MDLS_PERSIST");
     return v && v[0] == '1';
-  }() && pro;
+  }() && pro && M == 2;  // the persistent kernel is instantiated for dd only
   auto fork = [](cudaStream_t from, cudaStream_t to) {
     cudaEvent_t ev = pool_event();
     cudaEventRecord(ev, from);
