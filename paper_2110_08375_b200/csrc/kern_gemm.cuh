@@ -184,6 +184,62 @@ void gemm(cudaStream_t st, int64_t m, int64_t n, int64_t k, CMat A, CMat B, Mat 
   }
 }
 
+// ---------------------------------------------------------------------------
+// X = -T^T (Y^T C) for a leaf's trailing update without forming W = -Y T:
+// the split-K partials of Z = Y^T C (B x n) are summed (exact accumulator
+// merges, fixed order) and multiplied by -T^T (T: B x B upper, ld 32) in one
+// kernel; a CTA = 16 columns x B rows.  X then feeds C += Y X.
+// ---------------------------------------------------------------------------
+template <int M, int B>
+__global__ void __launch_bounds__(16 * B) splitk_reduce_t_kernel(int64_t n, int64_t S, const double* __restrict__ part,
+                                                                 CMat T, double* X, int64_t ldx, int64_t psx) {
+  __shared__ md<M> Z[16][B];
+  const int p = threadIdx.x % B, jl = threadIdx.x / B;
+  const int64_t j = (int64_t)blockIdx.x * 16 + jl;
+  const int64_t pps = (int64_t)B * n * S;
+  if (j < n) {
+    Acc<M> acc;
+    acc.init();
+    for (int64_t z = 0; z < S; ++z) {
+      const md<M> pz = ld<M>(part, pps, p + (j + z * n) * B);
+      Acc<M> o;
+#pragma unroll
+      for (int k = 0; k < Acc<M>::NV; ++k) o.r(k) = (k < M) ? pz.v[k] : 0.0;
+      acc.merge(o);
+    }
+    Z[jl][p] = acc.get();
+  }
+  __syncthreads();
+  if (j < n) {
+    Acc<M> acc;
+    acc.init();
+    for (int q = 0; q <= p; ++q) acc.add_prod(ld<M>(T.p, T.ps, q + (int64_t)p * T.ld), Z[jl][q]);
+    st<M>(X, psx, p + j * ldx, neg(acc.get()));
+  }
+}
+
+// X (B x n) = -T^T (Y^T C): Y r x B, C r x n (both column-major), X with ld B
+template <int M>
+void leaf_t_product(cudaStream_t st, int B, int64_t n, int64_t r, CMat Y, CMat T, CMat C, Mat X, double* part,
+                    int64_t part_cap_elems) {
+  using Tl = GemmTile<M, 2>;
+  const int64_t tiles = cdiv(B, Tl::BM) * cdiv(n, Tl::BN);
+  const int64_t target = 2 * kNumSMs;
+  int64_t S = std::min<int64_t>(kMaxSplitK, std::max<int64_t>(1, cdiv(target, tiles)));
+  S = std::max<int64_t>(1, std::min<int64_t>(S, r / (2 * Tl::BK)));
+  while (S > 1 && (int64_t)B * n * S > part_cap_elems) --S;
+  const int64_t kc = cdiv(cdiv(r, S), Tl::BK) * Tl::BK;
+  S = std::max<int64_t>(1, cdiv(r, kc));
+  GemmArgs g{B, n, r, Y.p, Y.ld, Y.ps, C.p, C.ld, C.ps, nullptr, B, 0, 0, kc, part, S};
+  dim3 grid((unsigned)cdiv(n, Tl::BN), (unsigned)cdiv(B, Tl::BM), (unsigned)S);
+  MDLS_LAUNCH(F_GEMM, st, gemm_kernel<M, 2, true, false><<<grid, Tl::NT, 0, st>>>(g));
+  if (B == 16)
+    MDLS_LAUNCH(F_GEMM, st, splitk_reduce_t_kernel<M, 16><<<(unsigned)cdiv(n, 16), 256, 0, st>>>(n, S, part, T, X.p, X.ld, X.ps));
+  else
+    MDLS_LAUNCH(F_GEMM, st, splitk_reduce_t_kernel<M, 8><<<(unsigned)cdiv(n, 16), 128, 0, st>>>(n, S, part, T, X.p, X.ld, X.ps));
+}
+
+
 // Load every md GEMM kernel of this precision/transposition now.  With CUDA's lazy module
 // loading, a kernel's first launch loads it, which must not happen while the persistent leaf
 // chain (solver.cuh::qr_factor_chain) waits for work on other streams.
@@ -195,10 +251,21 @@ void gemm_preload() {
   cudaFuncGetAttributes(&fa, gemm_kernel<M, 2, TA, TB>);
   cudaFuncGetAttributes(&fa, gemm_kernel<M, 3, TA, TB>);
   cudaFuncGetAttributes(&fa, splitk_reduce_kernel<M>);
+  cudaFuncGetAttributes(&fa, splitk_reduce_t_kernel<M, 16>);
+  cudaFuncGetAttributes(&fa, splitk_reduce_t_kernel<M, 8>);
 }
+
+// leaf_t_product is instantiated once per precision (with the TA = true, TB = false GEMM)
+#define MDLS_INSTANTIATE_LEAF_T(MM, TA, TB) MDLS_INSTANTIATE_LEAF_T_##TA##_##TB(MM)
+#define MDLS_INSTANTIATE_LEAF_T_true_false(MM) \
+  template void leaf_t_product<MM>(cudaStream_t, int, int64_t, int64_t, CMat, CMat, CMat, Mat, double*, int64_t);
+#define MDLS_INSTANTIATE_LEAF_T_false_true(MM)
+#define MDLS_INSTANTIATE_LEAF_T_false_false(MM)
+#define MDLS_INSTANTIATE_LEAF_T_true_true(MM)
 
 #define MDLS_INSTANTIATE_GEMM(MM, TA, TB)                                                                   \
   template void gemm<MM, TA, TB>(cudaStream_t, int64_t, int64_t, int64_t, CMat, CMat, Mat, int, double*, int64_t); \
-  template void gemm_preload<MM, TA, TB>();
+  template void gemm_preload<MM, TA, TB>();                                                                   \
+  MDLS_INSTANTIATE_LEAF_T(MM, TA, TB)
 
 }  // namespace mdls

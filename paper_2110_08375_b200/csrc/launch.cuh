@@ -14,6 +14,9 @@ void gemm(cudaStream_t st, int64_t m, int64_t n, int64_t k, CMat A, CMat B, Mat 
 
 template <int M, bool TA, bool TB>
 void gemm_preload();
+template <int M>
+void leaf_t_product(cudaStream_t st, int B, int64_t n, int64_t r, CMat Y, CMat T, CMat C, Mat X, double* part,
+                    int64_t part_cap_elems);
 void flags_preload();  // ledger.cu
 
 template <int M>

@@ -363,6 +363,15 @@ cudaError_t qr_factor_chain(cudaStream_t st, int64_t Mr, int64_t K, int64_t nb, 
       done = launch_leaf_apply<M>(Las, Mr, js, B, A, b.Y, Ts, c0, K) == cudaSuccess;
       if (!done) cudaGetLastError();
     }
+    if (!done && pro && c0 < K && (B == 16 || B == 8)) {
+      // X = -T_s^T (Y_s^T C): no W_s on this stream (the T product is folded into the split-K reduction)
+      set_stage(MDLS_ST_TRAILING);
+      const Mat Cm = sub(A, js, c0);
+      const Mat Xb{La.X.p, B, La.X.ps};
+      leaf_t_product<M>(Las, B, K - c0, r, Ys, cm(Ts), cm(Cm), Xb, La.part, La.cap);
+      gemm<M, false, false>(Las, r, K - c0, B, Ys, cm(Xb), Cm, 1, nullptr, 0);
+      done = true;
+    }
     if (!done) {
       set_stage(MDLS_ST_WY);
       if (pro) gemm<M, false, false>(Las, r, B, B, Ys, cm(Ts), Wls, 3, nullptr, 0);  // W_s = -Y_s T_s
