@@ -54,18 +54,19 @@ void set_stage(int stage) { t_stage = stage; }
 // two library-owned non-blocking side streams per device (joined into the
 // caller's stream by events in every call, so graph capture and ordering hold)
 cudaStream_t side_stream(int which) {
-  // 0, 1: high priority (QR critical chain, trailing applies it waits on); 2, 3: low (W build, Q, inversion)
+  // 0, 1, 4: high priority (QR critical chain, trailing applies it waits on); 2, 3, 5: low (W build, Q, inversion)
   static std::mutex mu;
-  static std::vector<cudaStream_t> streams;  // [device * 4 + which]
+  static std::vector<cudaStream_t> streams;  // [device * 6 + which]
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lk(mu);
-  const size_t idx = (size_t)dev * 4 + (which & 3);
+  const size_t idx = (size_t)dev * 6 + (size_t)(which % 6);
   if (streams.size() <= idx) streams.resize(idx + 1, nullptr);
   if (!streams[idx]) {
     int least = 0, greatest = 0;
     cudaDeviceGetStreamPriorityRange(&least, &greatest);
-    cudaStreamCreateWithPriority(&streams[idx], cudaStreamNonBlocking, (which & 3) < 2 ? greatest : least);
+    const int w = which % 6;
+    cudaStreamCreateWithPriority(&streams[idx], cudaStreamNonBlocking, (w < 2 || w == 4) ? greatest : least);
   }
   return streams[idx];
 }

@@ -258,7 +258,11 @@ cudaError_t qr_factor_chain(cudaStream_t st, int64_t Mr, int64_t K, int64_t nb, 
     cudaEventRecord(ev, from);
     cudaStreamWaitEvent(to, ev, 0);
   };
-  cudaStream_t Lc = side_stream(0), Las = side_stream(1), Lws = side_stream(2), Lqs = side_stream(3);
+  static const bool q_high = [] {  // MDLS_Q_PRIO=high: forward Q on a high-priority stream
+    const char* v = getenv("MDLS_Q_PRIO");
+    return v && v[0] == 'h';
+  }();
+  cudaStream_t Lc = side_stream(0), Las = side_stream(1), Lws = side_stream(2), Lqs = side_stream(q_high ? 4 : 3);
   const Lane La = b.lane(0, Las), Lw = b.lane(1, Lws), Lq = b.lane(2, Lqs);
   if (persist) {
     static bool loaded = false;  // lazy module loading must not happen while the chain spins
