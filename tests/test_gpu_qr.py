@@ -127,3 +127,21 @@ def test_lstsq_config2_full(orc, mdls, dev, prec):
     print(f"config 2/3 {prec}: x err/tol = {err / tol:.3e}, R worst column err/tol = {rr:.3e}")
     assert err <= tol, (err, tol)
     assert rr <= 1.0
+
+
+@pytest.mark.parametrize("prec,M,K,nb", [("dd", 1536, 1024, 128), ("qd", 1280, 256, 64), ("dd", 2048, 128, 16),
+                                        ("od", 1100, 64, 8)])
+def test_lstsq_tall_512_thread_leaf(orc, mdls, dev, prec, M, K, nb):
+    """Overdetermined systems taller than 1024 rows: the register leaf's 512-thread variant (rows per CTA in
+    (64, 128]) in the chained factorisation, plus the residual entries of Q^T b."""
+    A, b = inputs.lstsq_problem(M, K, prec, 3)
+    r = mdls.lstsq(prec, _gpu(A, dev), _gpu(b, dev), nb, form_q=True, want_R=True, want_y=True)
+    torch.cuda.synchronize()
+    assert int(r.info.item()) == 0
+    xo, Ro, yo = orc.lstsq(prec, A, b)
+    err, tol = vec_ok(orc, prec, r.x.cpu().numpy(), xo, K)
+    assert err <= tol, (err, tol)
+    assert mat_cols_ok(orc, prec, r.R.cpu().numpy(), Ro, K) <= 1.0
+    # |Q^T b| beyond K = residual norm: compare the sum of squares of the tail in fp64 (leading limbs)
+    yg = r.y.cpu().numpy()
+    assert abs(np.linalg.norm(yg[0, K:]) - np.linalg.norm(yo[0, K:])) <= 1e-12 * max(1.0, np.linalg.norm(yo[0, K:]))
