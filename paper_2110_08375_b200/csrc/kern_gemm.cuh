@@ -34,7 +34,9 @@ __global__ void __launch_bounds__(GemmTile<M, V>::NT) gemm_kernel(GemmArgs g) {
   __shared__ double Bs[M][BK][BN];
 
   const int tid = threadIdx.x;
-  const int tx = tid % NX, ty = tid / NX;
+  // consecutive lanes own consecutive output ROWS: the epilogue's C loads/stores and the split-K
+  // partial stores are coalesced along the column-major planes (they dominate when k is small)
+  const int ty = tid % NY, tx = tid / NY;
   const int64_t i0 = (int64_t)blockIdx.y * BM, j0 = (int64_t)blockIdx.x * BN;
   const int64_t kb = (int64_t)blockIdx.z * g.kc;
   const int64_t ke = min(g.k, kb + g.kc);
