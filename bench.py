@@ -46,7 +46,7 @@ FP64_PIPE_TOPS = 148 * 64 * 1.965e9 / 1e12            # 18.6 FP64-pipe lane ops/
 OPS_PER_PAIR = {"dd": 12, "qd": 116, "od": 970}
 # dram traffic per launch of the roofline GEMM (1024 x 1024 x 128, C += X Y^T) from one ncu --set full
 # capture (tools/prof_gemm.py; profiles/r01_ncu_gemm_roofline.txt), bytes read + written, per precision
-GEMM_NCU_TRAFFIC = {"dd": 4294912 + 81408, "qd": 42001920 + 156672, "od": 83991040 + 14889472}
+GEMM_NCU_TRAFFIC = {"dd": 4240384 + 2560, "qd": 42001664 + 119040, "od": 84171776 + 14920192}
 # paper's V100 times for the same least-squares workload (T11): QR + BS kernel ms
 PAPER_V100_MS = {"dd": 451.1 + 4.0, "qd": 3020.6 + 28.0, "od": 11924.5 + 114.5}
 L2_FLUSH_BYTES = 512 << 20

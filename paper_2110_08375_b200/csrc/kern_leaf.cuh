@@ -544,7 +544,7 @@ __device__ __forceinline__ void leaf_prologue(const LeafArgs<M>& a, cg::cluster_
   constexpr int RS0 = (NT / BB) >= 1 ? NT / BB : 1;
   const int Rxp = (Rx + 4 * RS0 - 1) / (4 * RS0) * (4 * RS0);
   for (int e = tid; e < Rxp * B; e += NT) {
-    const int i = e / B, p = e % B;
+    const int i = e % Rxp, p = e / Rxp;  // consecutive threads walk a column: coalesced global loads
     const int64_t g = (i < ex) ? a.jsp + rank + (int64_t)i * C : row0 + (i - ex);
     md<M> y = md_zero<M>(), c = md_zero<M>();
     if (i < Rx) {
