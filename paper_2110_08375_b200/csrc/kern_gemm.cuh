@@ -125,6 +125,7 @@ __global__ void splitk_reduce_kernel(int64_t m, int64_t n, int64_t S, const doub
     const md<M> p0 = ld<M>(part, pps, e);
 #pragma unroll
     for (int k = 0; k < Acc<M>::NV; ++k) acc.r(k) = (k < M) ? p0.v[k] : 0.0;
+#pragma unroll 4
     for (int64_t z = 1; z < S; ++z) {
       const md<M> pz = ld<M>(part, pps, i + (j + z * n) * m);
       Acc<M> o;
@@ -202,7 +203,8 @@ __global__ void __launch_bounds__(16 * B) splitk_reduce_t_kernel(int64_t n, int6
   if (j < n) {
     Acc<M> acc;
     acc.init();
-    for (int64_t z = 0; z < S; ++z) {
+#pragma unroll 4
+    for (int64_t z = 0; z < S; ++z) {  // unrolled: the partial loads are issued ahead of the merges
       const md<M> pz = ld<M>(part, pps, p + (j + z * n) * B);
       Acc<M> o;
 #pragma unroll
