@@ -1,5 +1,7 @@
 // kern_gemm.cuh -- md GEMM on the FP64 pipe (trailing update, WY build, Q formation, Q^T b).
 #pragma once
+#include <cstdlib>
+
 #include "types.cuh"
 
 namespace mdls {
@@ -181,7 +183,11 @@ void gemm(cudaStream_t st, int64_t m, int64_t n, int64_t k, CMat A, CMat B, Mat 
     const int64_t t0 = cdiv(m, GemmTile<M, 0>::BM) * cdiv(n, GemmTile<M, 0>::BN);
     const bool can_split = part && k >= 8 * GemmTile<M, 0>::BK;
     // the large tile once it fills about a wave (2 CTAs per SM resident), or with split-K
-    if (t0 >= (2 * kNumSMs) / 3 || (can_split && t0 >= target / 8))
+    static const int64_t v0_min = [] {  // MDLS_GEMM_V0_MIN: tiles needed for the large tile (tuning)
+      const char* v = getenv("MDLS_GEMM_V0_MIN");
+      return (int64_t)(v ? atoi(v) : (2 * kNumSMs) / 3);
+    }();
+    if (t0 >= v0_min || (can_split && t0 >= target / 8))
       gemm_launch<M, 0, TA, TB>(st, m, n, k, A, B, C, mode, part, part_cap_elems);
     else gemm_launch<M, 1, TA, TB>(st, m, n, k, A, B, C, mode, part, part_cap_elems);
   }
