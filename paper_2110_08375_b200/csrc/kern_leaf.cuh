@@ -726,10 +726,10 @@ __device__ __forceinline__ void leaf_body(const LeafArgs<M>& a, bool init_bars, 
   __shared__ __align__(16) md<M> pvl[B];            // pivot row staging in the owner CTA
   __shared__ __align__(8) unsigned long long bar[2];
   __shared__ Acc<M> wpart[NW][B];
-  __shared__ md<M> G[B], W[B], betas[B];
+  __shared__ md<M> G[B], W[B], betas[B], Uc[B], Qc[B];
   __shared__ md<M> SY[B][B];  // SY[p][l] = Y_p^T v_l (p < l)
   __shared__ md<M> Ts[B][B];
-  __shared__ md<M> sc_mu, sc_rs, sc_rsig, sc_rmu, sc_rv1;
+  __shared__ md<M> sc_mu, sc_rs, sc_rsig, sc_rmu, sc_rv1, sc_s, sc_bq;
 
   const int64_t total = a.Mrows - a.js;
   const int64_t row0 = a.js + (int64_t)rank * a.R;
@@ -870,11 +870,12 @@ __device__ __forceinline__ void leaf_body(const LeafArgs<M>& a, bool init_bars, 
         }
       }
     } else {
+      // qd/od, phase A: mu and s = x1 +- mu (thread 0), 1/sigma (warp 1), 1/mu = rsqrt(x1^2 + sigma) (warp 2)
       if (!deg) {
         if (tid == 0) {
           const md<M> mu = sqrt_fast<M>(add<M>(mul<M>(x1, x1), sigma));
           sc_mu = mu;
-          sc_rs = recip_fast<M>(pos ? add<M>(x1, mu) : sub<M>(x1, mu));
+          sc_s = pos ? add<M>(x1, mu) : sub<M>(x1, mu);
         } else if (tid == 32) {
           if (pos) sc_rsig = recip_fast<M>(sigma);
         } else if (tid == 64) {
@@ -888,25 +889,50 @@ __device__ __forceinline__ void leaf_body(const LeafArgs<M>& a, bool init_bars, 
     __syncthreads();
     LEAF_MARK(l, 5);
     if constexpr (M != 2) {
-      // (5) beta, 1/v1 and u_c / w_c once per column (B threads, no divergent arithmetic)
+      // phase B: thread 0 forms rs = 1/s (the long reciprocal) while warp 1 prepares everything that does
+      // not need it -- x1 > 0: 1/v1 = -s/sigma, u_c = a_jc + g_c/v1, q_c = sigma (1/mu) u_c, so that after
+      // rs only w_c = rs q_c and beta = rs (sigma/mu) remain; x1 <= 0: beta = -v1/mu (v1 = s).
+      if (!deg && tid == 0) sc_rs = recip_fast<M>(sc_s);
+      if (tid >= 32 && tid < 32 + B && !deg) {
+        const int c = tid - 32;
+        const md<M> sv = sc_s, rmu = sc_rmu;
+        if (pos) {
+          const md<M> rv1 = neg(mul<M>(sv, sc_rsig));
+          const md<M> pc = piv[buf][c];
+          const md<M> u = add<M>(pc, mul<M>(rv1, G[c]));
+          const md<M> bq = mul<M>(sigma, rmu);
+          Uc[c] = u;
+          Qc[c] = mul<M>(bq, u);
+          if (c == 0) {
+            sc_rv1 = rv1;
+            sc_bq = bq;
+          }
+        } else if (c == 0) {
+          sc_bq = neg(mul<M>(sv, rmu));  // beta itself for x1 <= 0
+        }
+      }
+      __syncthreads();
+      // phase C: beta, u_c / w_c once per column (B threads)
       if (tid < B) {
         const int c = tid;
-        const md<M> mu = sc_mu;
-        md<M> beta, rv1;
+        const md<M> pc = piv[buf][c];
+        md<M> beta, u, w;
         if (deg) {
           beta = md_zero<M>();
-          rv1 = md_from<M>(1.0);
+          u = pc;
+          w = md_zero<M>();
+          if (c == 0) sc_rv1 = md_from<M>(1.0);
         } else if (pos) {
-          rv1 = neg(mul<M>(add<M>(x1, mu), sc_rsig));
-          beta = mul<M>(mul<M>(sigma, sc_rs), sc_rmu);
+          beta = mul<M>(sc_rs, sc_bq);
+          u = Uc[c];
+          w = mul<M>(sc_rs, Qc[c]);
         } else {
-          rv1 = sc_rs;
-          beta = neg(mul<M>(sub<M>(x1, mu), sc_rmu));
+          const md<M> rv1 = sc_rs;
+          beta = sc_bq;
+          u = add<M>(pc, mul<M>(rv1, G[c]));
+          w = mul<M>(beta, u);
+          if (c == 0) sc_rv1 = rv1;
         }
-        if (c == 0) sc_rv1 = rv1;
-        const md<M> pc = piv[buf][c];
-        const md<M> u = deg ? pc : add<M>(pc, mul<M>(rv1, G[c]));
-        const md<M> w = mul<M>(beta, u);
         if (c < l) SY[c][l] = u;
         else if (c == l) betas[l] = beta;
         W[c] = (c > l && !deg) ? w : md_zero<M>();
