@@ -173,6 +173,11 @@ int mdls_trace_collect(double *stage_ms, double *family_ms, int64_t *family_laun
                      double *Q_out, int64_t ldq, int64_t psq, double *y_out, int64_t psy, void *work,              \
                      size_t work_bytes, int *dev_info, void *stream);                                              \
                                                                                                                    \
+  /* ||y||_2 of the md vector y of length n (n >= 0), in md: one md number written to out (limb l at           \
+   * out[l*pso]).  With y = (Q^T b)(K+1:M) from mdls_lstsq's y_out this is the least-squares residual norm        \
+   * ||b - A x||_2 (orthogonality of Q).  Fixed-order reduction (bitwise reproducible). */  \
+  int mdls_norm2_##P(int64_t n, const double *y, int64_t psy, double *out, int64_t pso, void *stream);             \
+                                                                                                                   \
   /* multi-GPU building blocks (block-column sharded QR; host orchestration in sharded.py).           \
    * qr_panel: factor panel k, i.e. the columns [k*nb, (k+1)*nb) of A passed as the M x nb operand Ak (rows        \
    * 0..M-1, all earlier panels already applied), M >= (k+1)*nb; on return Ak holds R and v like mdls_qr, and     \

@@ -77,6 +77,10 @@ def _load(counting: bool = False) -> ctypes.CDLL:
     lib.oracle_inv_normal.argtypes = [ctypes.c_int, _I64, _I64, _D, _I64, _D, _D, ctypes.c_int]
     lib.oracle_inv_normal.restype = ctypes.c_double
     lib.oracle_dot.argtypes = [ctypes.c_int, _I64, _D, _I64, _I64, _D, _I64, _I64, _D]
+    lib.oracle_blocked.argtypes = [ctypes.c_int, ctypes.c_int, _I64, _I64, _I64, _D, _D, _D, _D, _D, _D,
+                                   ctypes.POINTER(_I64), ctypes.POINTER(_I64)]
+    lib.oracle_norm2.argtypes = [ctypes.c_int, _I64, _D, _I64, _D]
+    lib.oracle_residual_direct.argtypes = [ctypes.c_int, _I64, _I64, _D, _I64, _D, _D, _D]
     lib.oracle_count_get.argtypes = [ctypes.POINTER(ctypes.c_uint64)]
     lib.oracle_selfcheck.restype = ctypes.c_int
     if lib.oracle_selfcheck() != 0:
@@ -249,6 +253,26 @@ def lstsq(prec, A: np.ndarray, b: np.ndarray, nthreads: int = 0):
     return x, R, y
 
 
+def norm2(prec, y: np.ndarray) -> np.ndarray:
+    """||y||_2 of an (m, n) md vector, as an (m,) md number."""
+    m = _m_of(prec)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    out = np.zeros(m)
+    _load().oracle_norm2(m, y.shape[1], _p(y), y.shape[1], _p(out))
+    return out
+
+
+def residual_direct(prec, A: np.ndarray, x: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """||b - A x||_2 evaluated directly in md, as an (m,) md number."""
+    m = _m_of(prec)
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    _, K, M = A.shape
+    out = np.zeros(m)
+    _load().oracle_residual_direct(m, M, K, _p(A), M, _p(np.ascontiguousarray(x, dtype=np.float64)),
+                                   _p(np.ascontiguousarray(b, dtype=np.float64)), _p(out))
+    return out
+
+
 def _cols_arg(cols):
     if cols is None:
         return None, 0
@@ -291,3 +315,37 @@ def dot(prec, a: np.ndarray, b: np.ndarray) -> np.ndarray:
     out = np.zeros(m)
     _load().oracle_dot(m, n, _p(a), n, 1, _p(b), n, 1, _p(out))
     return out
+
+
+# --------------------------------------------------------------------------- blocked, counted pipelines
+STAGES = ("house", "panel", "wy", "trailing", "form_q", "qtb", "invert", "mulinv", "bsupdate")
+BLOCKED_OPS = {"qr": 0, "backsub": 1, "lstsq": 2, "apply_qt": 3, "lstsq_noq": 4}
+
+
+def blocked(op: str, prec, A: np.ndarray, b: np.ndarray, nb: int):
+    """Algorithm 2 (blocked Householder QR) / Algorithm 1 (tiled back substitution) step by step
+    with per-stage md-op counters (mdls_oracle.c ``oracle_blocked``).  A: (m, K, M), or the upper
+    triangular (m, K, K) for ``backsub``; b: (m, M).  Returns a dict with x, R, Q, y (None where the
+    op has none), ``counts`` {stage: {add, mul, div, sqrt}}, ``nonpos`` (columns that took GVL's
+    x1 <= 0 branch) and ``info``."""
+    m = _m_of(prec)
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    _, K, M = A.shape
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    code = BLOCKED_OPS[op]
+    x = np.zeros((m, K))
+    R = np.zeros((m, K, M)) if code in (0, 2, 4) else None
+    Q = np.zeros((m, M, M)) if code in (0, 2) else None
+    y = np.zeros((m, M)) if code in (2, 3, 4) else None
+    cnt = np.zeros((9, 4), dtype=np.int64)
+    nonpos = ctypes.c_int64(0)
+    nul = ctypes.POINTER(ctypes.c_double)()
+    info = _load().oracle_blocked(code, m, M, K, nb, _p(A), _p(b), _p(x), _p(R) if R is not None else nul,
+                                  _p(Q) if Q is not None else nul, _p(y) if y is not None else nul,
+                                  cnt.ctypes.data_as(ctypes.POINTER(_I64)), ctypes.byref(nonpos))
+    if info < 0:
+        raise ValueError(f"oracle_blocked rc={info}")
+    counts = {s: {"add": int(cnt[i, 0]), "mul": int(cnt[i, 1]), "div": int(cnt[i, 2]), "sqrt": int(cnt[i, 3])}
+              for i, s in enumerate(STAGES)}
+    return {"x": x if code != 3 and code != 0 else None, "R": R, "Q": Q, "y": y, "counts": counts,
+            "nonpos": int(nonpos.value), "info": int(info)}

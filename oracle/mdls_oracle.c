@@ -655,6 +655,43 @@ int oracle_dot(int m, int64_t n, const double *a, int64_t pa, int64_t sa, const 
   return 0;
 }
 
+/* ||y||_2 in md: s = sum_i y_i^2 ascending from 0, then md sqrt (the residual norm of SPEC S:448 when
+ * y = (Q^T b)(K+1:M)) */
+int oracle_norm2(int m, int64_t n, const double *y, int64_t psy, double *out) {
+  if (m != 2 && m != 4 && m != 8) return -2;
+  double s[MAXM], t[MAXM], v[MAXM];
+  md_zero(m, s);
+  for (int64_t i = 0; i < n; ++i) {
+    for (int k = 0; k < m; ++k) v[k] = y[k * psy + i];
+    md_mul(m, v, v, t);
+    md_add(m, s, t, s);
+  }
+  md_sqrt(m, s, out);
+  return 0;
+}
+
+/* ||b - A x||_2 in md, evaluated directly: r_i = b_i - sum_j A_ij x_j (ascending j), then oracle_norm2 */
+int oracle_residual_direct(int m, int64_t M, int64_t K, const double *Ap, int64_t lda, const double *x,
+                           const double *b, double *out) {
+  if (m != 2 && m != 4 && m != 8) return -2;
+  mat_t A = {(double *)Ap, lda, K, m};
+  double *r = malloc(sizeof(double) * m * M);
+  for (int64_t i = 0; i < M; ++i) {
+    double s[MAXM], t[MAXM], a[MAXM], xx[MAXM];
+    for (int k = 0; k < m; ++k) s[k] = b[k * M + i];
+    for (int64_t j = 0; j < K; ++j) {
+      get(&A, i, j, a);
+      for (int k = 0; k < m; ++k) xx[k] = x[k * K + j];
+      md_mul(m, a, xx, t);
+      md_sub(m, s, t, s);
+    }
+    for (int k = 0; k < m; ++k) r[k * M + i] = s[k];
+  }
+  int rc = oracle_norm2(m, M, r, M, out);
+  free(r);
+  return rc;
+}
+
 /* ------------------------------------------------------------------------- */
 /* least squares: A = QR (A copied), y = Q^T b (reflectors), R x = y(1:K)      */
 /* ------------------------------------------------------------------------- */
@@ -791,6 +828,397 @@ double oracle_inv_normal(int m, int64_t M, int64_t K, const double *Ap, int64_t 
   free(r);
   double den = anorm * (anorm * xnorm + bnorm);
   return den > 0 ? worst / den : worst;
+}
+
+/* ------------------------------------------------------------------------- */
+/* BLOCKED algorithms with per-stage md-operation counters (the A10 ledger     */
+/* pin).  The paper accumulates, per kernel, the md operations it executes and */
+/* prices them with Table 1.  These functions carry out Algorithm 2 */
+/* (blocked Householder QR) and Algorithm 1 (tiled back             */
+/* substitution) step by step in the paper's order and count every  */
+/* md add/sub, mul, div and sqrt per stage.  They are single threaded (the     */
+/* counters are plain globals) and slow; they serve the ledger pin and the     */
+/* blocked == unblocked check (same result in exact        */
+/* arithmetic).  Readings: Householder vector scaled by one        */
+/* reciprocal 1/v1 then multiplications (Z5, the GPU's choice); every sum      */
+/* accumulates from 0 unless it updates an existing entry; the trailing update */
+/* is Y (W^T C), never forming Y W^T; Q backward; tile inverses exploit zeros. */
+/* ------------------------------------------------------------------------- */
+enum { ST_HOUSE, ST_PANEL, ST_WY, ST_TRAILING, ST_FORM_Q, ST_QTB, ST_INVERT, ST_MULINV, ST_BSUPDATE, N_ST };
+static int64_t g_mdc[N_ST][4]; /* add (incl. sub), mul, div, sqrt per stage */
+static int g_st;
+static void c_add(int m, const double *a, const double *b, double *c) { g_mdc[g_st][0]++; md_add(m, a, b, c); }
+static void c_sub(int m, const double *a, const double *b, double *c) { g_mdc[g_st][0]++; md_sub(m, a, b, c); }
+static void c_mul(int m, const double *a, const double *b, double *c) { g_mdc[g_st][1]++; md_mul(m, a, b, c); }
+static void c_div(int m, const double *a, const double *b, double *c) { g_mdc[g_st][2]++; md_div(m, a, b, c); }
+static void c_sqrt(int m, const double *a, double *c) { g_mdc[g_st][3]++; md_sqrt(m, a, c); }
+
+/* dense md matrix of r x c, contiguous m-limb records, column-major (scratch) */
+#define EL(P, ld, i, j) (&(P)[(((int64_t)(j)) * (ld) + (i)) * m])
+
+/* GVL Alg. 5.1.1 with the reciprocal reading (Z5): v = x * (1/v1).  Counts in
+ * the current stage.  Returns 1 when the x1 <= 0 branch was taken (no division
+ * for v1) and sigma != 0, else 0. */
+static int bhouse(int m, int64_t n, const double *x, double *v, double *beta, double *mu) {
+  double sigma[MAXM], t[MAXM];
+  md_zero(m, sigma);
+  for (int64_t i = 1; i < n; ++i) {
+    c_mul(m, &x[i * m], &x[i * m], t);
+    c_add(m, sigma, t, sigma);
+  }
+  md_set_d(m, 1.0, &v[0]);
+  if (md_lead(sigma) == 0.0) { /* P = I (GVL: beta = 0) */
+    for (int64_t i = 1; i < n; ++i) md_copy(m, &x[i * m], &v[i * m]);
+    md_zero(m, beta);
+    md_copy(m, &x[0], mu);
+    return 0;
+  }
+  double x1sq[MAXM], v1[MAXM], v1sq[MAXM], num[MAXM], den[MAXM], two[MAXM], one[MAXM], rv1[MAXM];
+  int nonpos = 0;
+  c_mul(m, &x[0], &x[0], x1sq);
+  c_add(m, x1sq, sigma, t);
+  c_sqrt(m, t, mu);
+  if (md_lead(&x[0]) <= 0.0) {
+    c_sub(m, &x[0], mu, v1);
+    nonpos = 1;
+  } else {
+    double ns[MAXM];
+    md_neg(m, sigma, ns);
+    c_add(m, &x[0], mu, t);
+    c_div(m, ns, t, v1);
+  }
+  c_mul(m, v1, v1, v1sq);
+  md_set_d(m, 2.0, two);
+  c_mul(m, two, v1sq, num);
+  c_add(m, sigma, v1sq, den);
+  c_div(m, num, den, beta);
+  md_set_d(m, 1.0, one);
+  c_div(m, one, v1, rv1);
+  for (int64_t i = 1; i < n; ++i) c_mul(m, &x[i * m], rv1, &v[i * m]);
+  return nonpos;
+}
+
+/* Algorithm 2 on F (M x K, limb-planar, ld M): R over F (v below the diagonal),
+ * Y and W of every panel kept in Yall / Wall (M x K dense records, panel k in
+ * rows j0.., columns j0..j0+nb-1), beta (K records).  *nonpos += columns that
+ * took the x1 <= 0 branch. */
+static void blocked_qr(int m, int64_t M, int64_t K, int64_t nb, mat_t *F, double *Yall, double *Wall, double *betas,
+                       int64_t *nonpos) {
+  const int64_t N = K / nb;
+  double *x = malloc(sizeof(double) * m * (M + 1)), *v = malloc(sizeof(double) * m * (M + 1));
+  double *tv = malloc(sizeof(double) * m * (nb + 1));
+  double *T = malloc(sizeof(double) * m * nb * (K + 1));
+  for (int64_t k = 0; k < N; ++k) {
+    const int64_t j0 = k * nb, r = M - j0, ct = K - j0 - nb;
+    /* step 1: for l = 1..n: v, beta; update R_kk */
+    for (int64_t l = 0; l < nb; ++l) {
+      const int64_t j = j0 + l, n = M - j;
+      for (int64_t i = 0; i < n; ++i) get(F, j + i, j, &x[i * m]);
+      double beta[MAXM], mu[MAXM];
+      g_st = ST_HOUSE;
+      *nonpos += bhouse(m, n, x, v, beta, mu);
+      g_st = ST_PANEL;
+      for (int64_t c = j + 1; c < j0 + nb; ++c) { /* beta R^T v, then R -= v w^T on the panel */
+        double s[MAXM], t[MAXM], a[MAXM], w[MAXM];
+        md_zero(m, s);
+        for (int64_t i = 0; i < n; ++i) {
+          get(F, j + i, c, a);
+          c_mul(m, &v[i * m], a, t);
+          c_add(m, s, t, s);
+        }
+        c_mul(m, beta, s, w);
+        for (int64_t i = 0; i < n; ++i) {
+          get(F, j + i, c, a);
+          c_mul(m, w, &v[i * m], t);
+          c_sub(m, a, t, a);
+          put(F, j + i, c, a);
+        }
+      }
+      put(F, j, j, mu);
+      for (int64_t i = 1; i < n; ++i) put(F, j + i, j, &v[i * m]);
+      md_copy(m, beta, &betas[j * m]);
+      /* Y(:, l) = v (rows j0.., zeros above row j) */
+      for (int64_t i = 0; i < r; ++i) {
+        if (i < l) md_zero(m, EL(Yall, M, j0 + i, j));
+        else md_copy(m, &v[(i - l) * m], EL(Yall, M, j0 + i, j));
+      }
+    }
+    /* step 2: W by z = -beta (v + W Y^T v), column by column */
+    g_st = ST_WY;
+    for (int64_t l = 0; l < nb; ++l) {
+      const int64_t j = j0 + l;
+      double nbeta[MAXM];
+      md_neg(m, &betas[j * m], nbeta);
+      for (int64_t p = 0; p < l; ++p) { /* t_p = Y_p^T v_l over the rows where v_l is nonzero */
+        double s[MAXM], t[MAXM];
+        md_zero(m, s);
+        for (int64_t i = l; i < r; ++i) {
+          c_mul(m, EL(Yall, M, j0 + i, j0 + p), EL(Yall, M, j0 + i, j), t);
+          c_add(m, s, t, s);
+        }
+        md_copy(m, s, &tv[p * m]);
+      }
+      for (int64_t i = 0; i < r; ++i) {
+        double u[MAXM], t[MAXM], z[MAXM];
+        md_zero(m, u);
+        for (int64_t p = 0; p < l; ++p) { /* u_i = (W t)_i */
+          c_mul(m, EL(Wall, M, j0 + i, j0 + p), &tv[p * m], t);
+          c_add(m, u, t, u);
+        }
+        c_add(m, EL(Yall, M, j0 + i, j), u, z); /* v + W Y^T v */
+        c_mul(m, nbeta, z, EL(Wall, M, j0 + i, j));
+      }
+    }
+    /* step 4: if k < N, R := R + Y (W^T C) on the trailing columns */
+    if (ct > 0) {
+      g_st = ST_TRAILING;
+      for (int64_t c = 0; c < ct; ++c) {
+        for (int64_t p = 0; p < nb; ++p) { /* T = W^T C */
+          double s[MAXM], t[MAXM], a[MAXM];
+          md_zero(m, s);
+          for (int64_t i = 0; i < r; ++i) {
+            get(F, j0 + i, j0 + nb + c, a);
+            c_mul(m, EL(Wall, M, j0 + i, j0 + p), a, t);
+            c_add(m, s, t, s);
+          }
+          md_copy(m, s, EL(T, nb, p, c));
+        }
+      }
+      for (int64_t c = 0; c < ct; ++c)
+        for (int64_t i = 0; i < r; ++i) { /* C += Y T */
+          double s[MAXM], t[MAXM];
+          get(F, j0 + i, j0 + nb + c, s);
+          for (int64_t p = 0; p < nb; ++p) {
+            c_mul(m, EL(Yall, M, j0 + i, j0 + p), EL(T, nb, p, c), t);
+            c_add(m, s, t, s);
+          }
+          put(F, j0 + i, j0 + nb + c, s);
+        }
+    }
+  }
+  free(x);
+  free(v);
+  free(tv);
+  free(T);
+}
+
+/* Q = P_WY(1) ... P_WY(N) backward: Q = I; for k = N..1: Q_tr += W_k (Y_k^T Q_tr),
+ * Q_tr = Q(j0:M, j0:M) (the paper forms Q forward; equal in exact arithmetic) */
+static void blocked_form_q(int m, int64_t M, int64_t K, int64_t nb, const double *Yall, const double *Wall, mat_t *Q) {
+  const int64_t N = K / nb;
+  for (int k = 0; k < m; ++k) memset(Q->p + (int64_t)k * Q->ld * Q->cols, 0, sizeof(double) * Q->ld * Q->cols);
+  for (int64_t i = 0; i < M; ++i) Q->p[i * Q->ld + i] = 1.0;
+  double *X = malloc(sizeof(double) * m * nb * (M + 1));
+  g_st = ST_FORM_Q;
+  for (int64_t k = N - 1; k >= 0; --k) {
+    const int64_t j0 = k * nb, r = M - j0;
+    for (int64_t c = 0; c < r; ++c)
+      for (int64_t p = 0; p < nb; ++p) { /* X = Y_k^T Q_tr */
+        double s[MAXM], t[MAXM], q[MAXM];
+        md_zero(m, s);
+        for (int64_t i = 0; i < r; ++i) {
+          get(Q, j0 + i, j0 + c, q);
+          c_mul(m, EL(Yall, M, j0 + i, j0 + p), q, t);
+          c_add(m, s, t, s);
+        }
+        md_copy(m, s, EL(X, nb, p, c));
+      }
+    for (int64_t c = 0; c < r; ++c)
+      for (int64_t i = 0; i < r; ++i) { /* Q_tr += W_k X */
+        double s[MAXM], t[MAXM];
+        get(Q, j0 + i, j0 + c, s);
+        for (int64_t p = 0; p < nb; ++p) {
+          c_mul(m, EL(Wall, M, j0 + i, j0 + p), EL(X, nb, p, c), t);
+          c_add(m, s, t, s);
+        }
+        put(Q, j0 + i, j0 + c, s);
+      }
+  }
+  free(X);
+}
+
+/* Algorithm 1 on the leading n x n of U (limb-planar, ld ldu,
+ * ucols columns): invert the N diagonal tiles (zeros exploited: column k of
+ * U_i^-1 solves U_i v = e_k, v_k = 1/u_kk, v_r = -(sum_{l=r+1..k} u_rl v_l) / u_rr
+ * with the reciprocals 1/u_rr formed once per tile), then for
+ * i = N..1: x_i = U_i^-1 b_i, b_j -= A_ji x_i (j < i).  Returns 0 or the 1-based
+ * first zero diagonal. */
+static int blocked_backsub(int m, int64_t n, int64_t nb, const mat_t *U, const double *y, double *x) {
+  const int64_t N = n / nb;
+  double *V = malloc(sizeof(double) * m * nb * nb * (N + 1)); /* tile i at V + i nb^2 m, nb x nb */
+  double *d = malloc(sizeof(double) * m * (nb + 1));
+  double *b = malloc(sizeof(double) * m * (n + 1));
+  int info = 0;
+  g_st = ST_INVERT;
+  for (int64_t ti = 0; ti < N; ++ti) {
+    const int64_t o = ti * nb;
+    double *Vi = V + ti * nb * nb * m;
+    double one[MAXM], u[MAXM];
+    md_set_d(m, 1.0, one);
+    for (int64_t rr = 0; rr < nb; ++rr) {
+      get(U, o + rr, o + rr, u);
+      if (u[0] == 0.0 && !info) info = (int)(o + rr + 1);
+      c_div(m, one, u, &d[rr * m]);
+    }
+    for (int64_t k = 0; k < nb; ++k) {
+      for (int64_t rr = k + 1; rr < nb; ++rr) md_zero(m, EL(Vi, nb, rr, k));
+      md_copy(m, &d[k * m], EL(Vi, nb, k, k));
+      for (int64_t rr = k - 1; rr >= 0; --rr) {
+        double s[MAXM], t[MAXM], ns[MAXM];
+        md_zero(m, s);
+        for (int64_t l = rr + 1; l <= k; ++l) {
+          get(U, o + rr, o + l, u);
+          c_mul(m, u, EL(Vi, nb, l, k), t);
+          c_add(m, s, t, s);
+        }
+        md_neg(m, s, ns);
+        c_mul(m, ns, &d[rr * m], EL(Vi, nb, rr, k));
+      }
+    }
+  }
+  for (int64_t i = 0; i < n; ++i)
+    for (int k = 0; k < m; ++k) b[i * m + k] = y[(int64_t)k * n + i];
+  for (int64_t ti = N - 1; ti >= 0; --ti) {
+    const int64_t o = ti * nb;
+    const double *Vi = V + ti * nb * nb * m;
+    g_st = ST_MULINV;
+    for (int64_t rr = 0; rr < nb; ++rr) { /* x_i = U_i^-1 b_i */
+      double s[MAXM], t[MAXM];
+      md_zero(m, s);
+      for (int64_t c = rr; c < nb; ++c) {
+        c_mul(m, EL(Vi, nb, rr, c), &b[(o + c) * m], t);
+        c_add(m, s, t, s);
+      }
+      for (int k = 0; k < m; ++k) x[(int64_t)k * n + o + rr] = s[k];
+    }
+    g_st = ST_BSUPDATE;
+    for (int64_t tj = 0; tj < ti; ++tj) /* b_j -= A_ji x_i */
+      for (int64_t rr = 0; rr < nb; ++rr) {
+        double *s = &b[(tj * nb + rr) * m], t[MAXM], a[MAXM], xx[MAXM];
+        for (int64_t c = 0; c < nb; ++c) {
+          get(U, tj * nb + rr, o + c, a);
+          for (int k = 0; k < m; ++k) xx[k] = x[(int64_t)k * n + o + c];
+          c_mul(m, a, xx, t);
+          c_sub(m, s, t, s);
+        }
+      }
+  }
+  free(V);
+  free(d);
+  free(b);
+  return info;
+}
+
+/* The blocked pipelines the ledger prices (op codes as MDLS_OP_* of include/mdls.h:
+ * 0 QR with Q formed, 1 BACKSUB, 2 LSTSQ = QR + Q + explicit Q^T b + BS, 3 APPLY_QT
+ * (Q^T b from the panels, after a QR whose counts are discarded), 4 LSTSQ_NOQ = QR +
+ * Q^T b from the panels + BS).  A: M x K (ld M) or, for BACKSUB, the upper
+ * triangular K x K; b: M (or K).  Outputs (nullable): x (K), R (M x K, strictly
+ * lower part zero), Q (M x M), y = Q^T b (M).  counts: int64[9][4] (add, mul, div,
+ * sqrt per stage, MDLS_ST_* order); nonpos: columns with x1 <= 0 and sigma != 0.
+ * Returns 0, a 1-based zero-diagonal row, or -1 for invalid arguments. */
+int oracle_blocked(int op, int m, int64_t M, int64_t K, int64_t nb, const double *A, const double *b, double *x,
+                   double *R_out, double *Q_out, double *y_out, int64_t *counts, int64_t *nonpos) {
+  if (m != 2 && m != 4 && m != 8) return -1;
+  if (nb < 1 || K < 1 || K % nb || (op != 1 && M < K) || op < 0 || op > 4) return -1;
+  memset(g_mdc, 0, sizeof(g_mdc));
+  int64_t np = 0;
+  int info = 0;
+  if (op == 1) {
+    mat_t U = {(double *)A, K, K, m};
+    double *xx = x ? x : malloc(sizeof(double) * m * K);
+    info = blocked_backsub(m, K, nb, &U, b, xx);
+    if (!x) free(xx);
+  } else {
+    double *F = malloc(sizeof(double) * m * M * K);
+    memcpy(F, A, sizeof(double) * m * M * K);
+    mat_t Fm = {F, M, K, m};
+    double *Yall = calloc((size_t)m * M * K, sizeof(double)), *Wall = calloc((size_t)m * M * K, sizeof(double));
+    double *betas = malloc(sizeof(double) * m * K);
+    blocked_qr(m, M, K, nb, &Fm, Yall, Wall, betas, &np);
+    double *Q = NULL;
+    if (op == 0 || op == 2) {
+      Q = Q_out ? Q_out : malloc(sizeof(double) * m * M * M);
+      mat_t Qm = {Q, M, M, m};
+      blocked_form_q(m, M, K, nb, Yall, Wall, &Qm);
+    }
+    if (op == 3) memset(g_mdc, 0, sizeof(g_mdc)); /* APPLY_QT prices only the application */
+    double *y = malloc(sizeof(double) * m * M);
+    if (op >= 2) {
+      g_st = ST_QTB;
+      if (op == 2) { /* explicit: y_c = sum_i Q_ic b_i */
+        mat_t Qm = {Q, M, M, m};
+        for (int64_t c = 0; c < M; ++c) {
+          double s[MAXM], t[MAXM], q[MAXM], bb[MAXM];
+          md_zero(m, s);
+          for (int64_t i = 0; i < M; ++i) {
+            get(&Qm, i, c, q);
+            for (int k = 0; k < m; ++k) bb[k] = b[(int64_t)k * M + i];
+            c_mul(m, q, bb, t);
+            c_add(m, s, t, s);
+          }
+          for (int k = 0; k < m; ++k) y[(int64_t)k * M + c] = s[k];
+        }
+      } else { /* by panels: y(j0:) += Y_k (W_k^T y(j0:)) */
+        memcpy(y, b, sizeof(double) * m * M);
+        mat_t Ym = {y, M, 1, m};
+        double *tv = malloc(sizeof(double) * m * (nb + 1));
+        for (int64_t k = 0; k < K / nb; ++k) {
+          const int64_t j0 = k * nb, r = M - j0;
+          for (int64_t p = 0; p < nb; ++p) {
+            double s[MAXM], t[MAXM], a[MAXM];
+            md_zero(m, s);
+            for (int64_t i = 0; i < r; ++i) {
+              get(&Ym, j0 + i, 0, a);
+              c_mul(m, EL(Wall, M, j0 + i, j0 + p), a, t);
+              c_add(m, s, t, s);
+            }
+            md_copy(m, s, &tv[p * m]);
+          }
+          for (int64_t i = 0; i < r; ++i) {
+            double s[MAXM], t[MAXM];
+            get(&Ym, j0 + i, 0, s);
+            for (int64_t p = 0; p < nb; ++p) {
+              c_mul(m, EL(Yall, M, j0 + i, j0 + p), &tv[p * m], t);
+              c_add(m, s, t, s);
+            }
+            put(&Ym, j0 + i, 0, s);
+          }
+        }
+        free(tv);
+      }
+      if (y_out) memcpy(y_out, y, sizeof(double) * m * M);
+    }
+    if (op == 2 || op == 4) { /* R(1:K, 1:K) x = y(1:K) by Algorithm 1 */
+      double *yk = malloc(sizeof(double) * m * K);
+      for (int k = 0; k < m; ++k) memcpy(yk + (int64_t)k * K, y + (int64_t)k * M, sizeof(double) * K);
+      double *Rk = malloc(sizeof(double) * m * K * K);
+      for (int k = 0; k < m; ++k)
+        for (int64_t j = 0; j < K; ++j)
+          for (int64_t i = 0; i < K; ++i)
+            Rk[(int64_t)k * K * K + j * K + i] = (i <= j) ? F[(int64_t)k * M * K + j * M + i] : 0.0;
+      mat_t U = {Rk, K, K, m};
+      double *xx = x ? x : malloc(sizeof(double) * m * K);
+      info = blocked_backsub(m, K, nb, &U, yk, xx);
+      if (!x) free(xx);
+      free(yk);
+      free(Rk);
+    }
+    if (R_out)
+      for (int k = 0; k < m; ++k)
+        for (int64_t j = 0; j < K; ++j)
+          for (int64_t i = 0; i < M; ++i)
+            R_out[(int64_t)k * M * K + j * M + i] = (i <= j) ? F[(int64_t)k * M * K + j * M + i] : 0.0;
+    if (Q && Q != Q_out) free(Q);
+    free(y);
+    free(F);
+    free(Yall);
+    free(Wall);
+    free(betas);
+  }
+  if (counts) memcpy(counts, g_mdc, sizeof(g_mdc));
+  if (nonpos) *nonpos = np;
+  return info;
 }
 
 /* runtime self-check of round-to-nearest-even without reassociation:

@@ -19,8 +19,8 @@ PRECISIONS = {"dd": 2, "qd": 4, "od": 8}
 OPS = {"add": 0, "sub": 1, "mul": 2, "div": 3, "sqrt": 4, "sqrt_fast": 5, "recip_fast": 6}
 T1_SUMS = {"dd": (20, 23, 70), "qd": (89, 336, 893), "od": (269, 1742, 5126)}  # P:102-136 (add, mul, div)
 
-__all__ = ["md_op", "qr", "apply_qt", "qt_b", "invert_tiles", "backsub", "lstsq", "counts", "workspace_bytes",
-           "PRECISIONS"]
+__all__ = ["md_op", "qr", "apply_qt", "qt_b", "invert_tiles", "backsub", "lstsq", "norm2", "counts",
+           "workspace_bytes", "PRECISIONS"]
 
 
 def _torch():
@@ -185,16 +185,27 @@ def backsub(prec: str, U, y, nb: int, n: int | None = None):
     return x, info
 
 
-class LstsqResult:
-    __slots__ = ("x", "R", "Q", "y", "info")
+def norm2(prec: str, y):
+    """||y||_2 of an (m, n) md vector, as an (m, 1) md tensor (mdls_norm2_<p>)."""
+    torch = _torch()
+    _check_md(y, prec, 2, "y")
+    out = torch.empty((PRECISIONS[prec], 1), dtype=torch.float64, device=y.device)
+    rc = _lib.fn("mdls_norm2_", prec)(y.shape[1], _ptr(y), y.shape[1], _ptr(out), 1, _stream())
+    _lib.check(rc, "norm2")
+    return out
 
-    def __init__(self, x, R, Q, y, info):
-        self.x, self.R, self.Q, self.y, self.info = x, R, Q, y, info
+
+class LstsqResult:
+    __slots__ = ("x", "R", "Q", "y", "info", "residual")
+
+    def __init__(self, x, R, Q, y, info, residual=None):
+        self.x, self.R, self.Q, self.y, self.info, self.residual = x, R, Q, y, info, residual
 
 
 def lstsq(prec: str, A, b, nb: int, form_q: bool = True, want_R: bool = False, want_Q: bool = False,
-          want_y: bool = False, work=None):
-    """Least squares x = argmin ||b - A x|| (QR, Q^T b, tiled back substitution)."""
+          want_y: bool = False, want_residual: bool = False, work=None):
+    """Least squares x = argmin ||b - A x|| (QR, Q^T b, tiled back substitution).  With want_residual the
+    result carries ``residual`` = ||(Q^T b)(K+1:M)||_2 = ||b - A x||_2 as an (m, 1) md tensor."""
     torch = _torch()
     _check_md(A, prec, 3, "A")
     _check_md(b, prec, 2, "b")
@@ -203,7 +214,7 @@ def lstsq(prec: str, A, b, nb: int, form_q: bool = True, want_R: bool = False, w
     x = torch.empty((m, K), dtype=torch.float64, device=dev)
     R = torch.empty((m, K, M), dtype=torch.float64, device=dev) if want_R else None
     Q = torch.empty((m, M, M), dtype=torch.float64, device=dev) if (want_Q and form_q) else None
-    y = torch.empty((m, M), dtype=torch.float64, device=dev) if want_y else None
+    y = torch.empty((m, M), dtype=torch.float64, device=dev) if (want_y or want_residual) else None
     op = _lib.OP_LSTSQ if form_q else _lib.OP_LSTSQ_NOQ
     if work is None:
         work, nbytes = _work(prec, op, M, K, nb, dev)
@@ -216,7 +227,8 @@ def lstsq(prec: str, A, b, nb: int, form_q: bool = True, want_R: bool = False, w
     rc = _lib.fn("mdls_lstsq_", prec)(M, K, nb, *_mat(A), *_vec(b), *_vec(x), int(form_q), *rp, *qp, *yp,
                                       _ptr(work), nbytes, _ptr(info), _stream())
     _lib.check(rc, "lstsq")
-    return LstsqResult(x, R, Q, y, info)
+    res = norm2(prec, y[:, K:].contiguous()) if want_residual else None
+    return LstsqResult(x, R, Q, y if want_y else None, info, res)
 
 
 def launch_count() -> int:

@@ -175,9 +175,8 @@ int MDLS_FN(mdls_qr_)(int64_t Mr, int64_t K, int64_t nb, double* A, int64_t lda,
   Mat Qm{Q, ldq, psq};
   const bool fwd = Q && q_forward<M>();
   if (use_chain<M>(Mr, K, nb)) {
-    if (qr_factor_chain<M>(st, Mr, K, nb, Am, b, Mat{at<double>(work, p.wl), Mr, Mr * K},
-                           Mat{at<double>(work, p.t), 32, 32 * std::max<int64_t>(K, 32)}, fwd ? &Qm : nullptr,
-                           at<int>(work, p.flags)) != cudaSuccess)
+    if (qr_factor_chain<M>(st, Mr, K, nb, Am, b, Mat{at<double>(work, p.t), 32, 32 * std::max<int64_t>(K, 32)},
+                           fwd ? &Qm : nullptr) != cudaSuccess)
       return MDLS_ERR_CUDA;
   } else if (qr_factor_overlap<M>(b.lane(0, st), b.lane(1, side_stream(0)), b.lane(2, side_stream(1)), Mr, K, nb, Am,
                                   b, fwd ? &Qm : nullptr) != cudaSuccess) {
@@ -225,6 +224,16 @@ int MDLS_FN(mdls_qt_b_)(int64_t Mr, int64_t Nc, const double* Q, int64_t ldq, in
   double* part = (work && work_bytes >= need) ? static_cast<double*>(work) : nullptr;
   gemm<M, true, false>(st, Nc, 1, Mr, CMat{Q, ldq, psq}, CMat{b, Mr, psb}, Mat{y, Nc, psy}, 0, part,
                        part ? kMaxSplit * Nc : 0);
+  return launched();
+}
+
+int MDLS_FN(mdls_norm2_)(int64_t n, const double* y, int64_t psy, double* out, int64_t pso, void* stream) {
+  if (n < 0) return -1;
+  if (!y || psy < n) return -2;
+  if (!out || pso < 1) return -4;
+  set_stage(MDLS_NSTAGES);
+  cudaStream_t st = S(stream);
+  MDLS_LAUNCH(F_MISC, st, norm2_kernel<M><<<1, 256, 0, st>>>(n, y, psy, out, pso));
   return launched();
 }
 
@@ -292,9 +301,8 @@ int MDLS_FN(mdls_lstsq_)(int64_t Mr, int64_t K, int64_t nb, const double* A, int
   Mat Q = (form_q && Q_out) ? Mat{Q_out, ldq, psq} : Mat{form_q ? at<double>(work, p.q) : nullptr, Mr, Mr * Mr};
   const bool fwd = form_q && q_forward<M>();
   if (use_chain<M>(Mr, K, nb)) {
-    if (qr_factor_chain<M>(st, Mr, K, nb, Af, bb, Mat{at<double>(work, p.wl), Mr, Mr * K},
-                           Mat{at<double>(work, p.t), 32, 32 * std::max<int64_t>(K, 32)}, fwd ? &Q : nullptr,
-                           at<int>(work, p.flags)) != cudaSuccess)
+    if (qr_factor_chain<M>(st, Mr, K, nb, Af, bb, Mat{at<double>(work, p.t), 32, 32 * std::max<int64_t>(K, 32)},
+                           fwd ? &Q : nullptr) != cudaSuccess)
       return MDLS_ERR_CUDA;
   } else if (qr_factor_overlap<M>(bb.lane(0, st), bb.lane(1, side_stream(0)), bb.lane(2, side_stream(1)), Mr, K, nb,
                                   Af, bb, fwd ? &Q : nullptr) != cudaSuccess) {

@@ -153,7 +153,7 @@ void gemm_launch(cudaStream_t st, int64_t m, int64_t n, int64_t k, CMat A, CMat 
                  int64_t part_cap_elems) {
   using Tl = GemmTile<M, V>;
   const int64_t tiles = cdiv(m, Tl::BM) * cdiv(n, Tl::BN);
-  const int64_t target = 2 * kNumSMs;
+  const int64_t target = 2 * num_sms();
   int64_t S = 1;
   if (part && tiles < target && k >= 4 * Tl::BK) {
     S = std::min<int64_t>(kMaxSplitK, cdiv(target, tiles));
@@ -174,7 +174,7 @@ template <int M, bool TA, bool TB>
 void gemm(cudaStream_t st, int64_t m, int64_t n, int64_t k, CMat A, CMat B, Mat C, int mode, double* part,
           int64_t part_cap_elems) {
   if (m <= 0 || n <= 0) return;
-  const int64_t target = 2 * kNumSMs;
+  const int64_t target = 2 * num_sms();
   if (m <= GemmTile<M, 2>::BM && n > m) {
     gemm_launch<M, 2, TA, TB>(st, m, n, k, A, B, C, mode, part, part_cap_elems);
   } else if (n <= GemmTile<M, 3>::BN && m > n) {
@@ -183,10 +183,7 @@ void gemm(cudaStream_t st, int64_t m, int64_t n, int64_t k, CMat A, CMat B, Mat 
     const int64_t t0 = cdiv(m, GemmTile<M, 0>::BM) * cdiv(n, GemmTile<M, 0>::BN);
     const bool can_split = part && k >= 8 * GemmTile<M, 0>::BK;
     // the large tile once it fills about a wave (2 CTAs per SM resident), or with split-K
-    static const int64_t v0_min = [] {  // MDLS_GEMM_V0_MIN: tiles needed for the large tile (tuning)
-      const char* v = getenv("MDLS_GEMM_V0_MIN");
-      return (int64_t)(v ? atoi(v) : (2 * kNumSMs) / 3);
-    }();
+    const int64_t v0_min = (2 * num_sms()) / 3;  // the large tile once it fills about 2/3 of a wave
     if (t0 >= v0_min || (can_split && t0 >= target / 8))
       gemm_launch<M, 0, TA, TB>(st, m, n, k, A, B, C, mode, part, part_cap_elems);
     else gemm_launch<M, 1, TA, TB>(st, m, n, k, A, B, C, mode, part, part_cap_elems);
@@ -234,7 +231,7 @@ void leaf_t_product(cudaStream_t st, int B, int64_t n, int64_t r, CMat Y, CMat T
                     int64_t part_cap_elems) {
   using Tl = GemmTile<M, 2>;
   const int64_t tiles = cdiv(B, Tl::BM) * cdiv(n, Tl::BN);
-  const int64_t target = 2 * kNumSMs;
+  const int64_t target = 2 * num_sms();
   int64_t S = std::min<int64_t>(kMaxSplitK, std::max<int64_t>(1, cdiv(target, tiles)));
   S = std::max<int64_t>(1, std::min<int64_t>(S, r / (2 * Tl::BK)));
   while (S > 1 && (int64_t)B * n * S > part_cap_elems) --S;
@@ -250,21 +247,6 @@ void leaf_t_product(cudaStream_t st, int B, int64_t n, int64_t r, CMat Y, CMat T
 }
 
 
-// Load every md GEMM kernel of this precision/transposition now.  With CUDA's lazy module
-// loading, a kernel's first launch loads it, which must not happen while the persistent leaf
-// chain (solver.cuh::qr_factor_chain) waits for work on other streams.
-template <int M, bool TA, bool TB>
-void gemm_preload() {
-  cudaFuncAttributes fa{};
-  cudaFuncGetAttributes(&fa, gemm_kernel<M, 0, TA, TB>);
-  cudaFuncGetAttributes(&fa, gemm_kernel<M, 1, TA, TB>);
-  cudaFuncGetAttributes(&fa, gemm_kernel<M, 2, TA, TB>);
-  cudaFuncGetAttributes(&fa, gemm_kernel<M, 3, TA, TB>);
-  cudaFuncGetAttributes(&fa, splitk_reduce_kernel<M>);
-  cudaFuncGetAttributes(&fa, splitk_reduce_t_kernel<M, 16>);
-  cudaFuncGetAttributes(&fa, splitk_reduce_t_kernel<M, 8>);
-}
-
 // leaf_t_product is instantiated once per precision (with the TA = true, TB = false GEMM)
 #define MDLS_INSTANTIATE_LEAF_T(MM, TA, TB) MDLS_INSTANTIATE_LEAF_T_##TA##_##TB(MM)
 #define MDLS_INSTANTIATE_LEAF_T_true_false(MM) \
@@ -275,7 +257,6 @@ void gemm_preload() {
 
 #define MDLS_INSTANTIATE_GEMM(MM, TA, TB)                                                                   \
   template void gemm<MM, TA, TB>(cudaStream_t, int64_t, int64_t, int64_t, CMat, CMat, Mat, int, double*, int64_t); \
-  template void gemm_preload<MM, TA, TB>();                                                                   \
   MDLS_INSTANTIATE_LEAF_T(MM, TA, TB)
 
 }  // namespace mdls

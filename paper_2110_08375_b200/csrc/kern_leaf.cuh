@@ -988,136 +988,10 @@ __device__ __forceinline__ void leaf_body(const LeafArgs<M>& a, bool init_bars, 
   cluster.sync();   // no CTA exits while another may still push into it
 }
 
-// ---------------------------------------------------------------------------
-// Trailing update of one leaf as ONE launch (A4 for the chained factorisation,
-// dd): C -= Y_s T_s^T (Y_s^T C) for the columns [c0, c1) of A, rows js..M-1,
-// where leaf s occupies columns js..js+B-1.  Each 16-CTA cluster owns B columns
-// and runs the leaf prologue on them (cluster reduce-scatter of Y_s^T C, T_s^T
-// product, DSMEM all-gather, row updates); blockIdx.y = column block.  Replaces
-// the W GEMM + split-K W^T C + reduction + Y X GEMM launch sequence.
-// ---------------------------------------------------------------------------
-template <int M, int B, int TPR, int NT>
-__global__ void __launch_bounds__(NT) leaf_apply_kernel(LeafArgs<M> a0, int64_t c0, int64_t c1) {
-  constexpr int V = B / TPR;
-  cg::cluster_group cluster = cg::this_cluster();
-  const int C = (int)cluster.num_blocks();
-  const int rank = (int)cluster.block_rank();
-  const int tid = threadIdx.x, h = tid % TPR, rg = tid / TPR;
-  const int64_t cb = c0 + (int64_t)blockIdx.y * B;  // this cluster's first column
-  // rows: the B rows of leaf s's diagonal block are the prologue's "rows above", tile rows start at js + B
-  LeafArgs<M> a = a0;
-  a.js = a0.jsp + B;                       // tile row start
-  a.A.p = a0.A.p + (cb - a.js) * a0.A.ld;  // column (a.js + p) of the shifted operand = column cb + p
-  const int64_t total = a.Mrows - a.js;
-  const int64_t row0 = a.js + (int64_t)rank * a.R;
-  int64_t Rp = total - (int64_t)rank * a.R;
-  Rp = Rp < 0 ? 0 : (Rp > a.R ? a.R : Rp);
-  const bool valid = rg < Rp;
-  const int64_t gi = row0 + rg;
-  const int ncols = (int)((c1 - cb) < (int64_t)B ? (c1 - cb) : (int64_t)B);
-  md<M> t[V];
-#pragma unroll
-  for (int q = 0; q < V; ++q) {
-    const int c = h * V + q;
-#pragma unroll
-    for (int k = 0; k < M; ++k)
-      t[q].v[k] = (valid && c < ncols) ? __ldcg(a.A.p + k * a.A.ps + (a.js + c) * a.A.ld + gi) : 0.0;
-  }
-  leaf_prologue<M, B, TPR, NT>(a, cluster, C, rank, t, Rp, valid, gi, row0, true, 0u, ncols);
-  if (valid) {
-#pragma unroll
-    for (int q = 0; q < V; ++q) {
-      const int c = h * V + q;
-      if (c < ncols) {
-#pragma unroll
-        for (int k = 0; k < M; ++k) a.A.p[k * a.A.ps + (a.js + c) * a.A.ld + gi] = t[q].v[k];
-      }
-    }
-  }
-  cluster.sync();  // no CTA exits while another may still push into it
-}
-
 template <int M, int B, int TPR, int NT>
 __global__ void __launch_bounds__(NT) leaf_reg_kernel(LeafArgs<M> a) {
   leaf_body<M, B, TPR, NT>(a, true, true, 0u);
 }
-
-// ---------------------------------------------------------------------------
-// Persistent leaf chain: ONE cluster launch factors every leaf of the matrix
-// in order (the only serial path of Algorithm 2), keeping its 16 SMs for the
-// whole factorisation instead of re-acquiring a free GPC for each of the
-// K/B leaves while the trailing / Q GEMMs flood the GPU.  Leaf s publishes
-// leaf_done[s] (release, after a device fence and a cluster barrier); before
-// leaf s >= 2 it waits for apply_done[s-2] (acquire), which the trailing-update
-// stream sets after applying leaf s-2 to every column beyond leaf s-1.
-// ---------------------------------------------------------------------------
-template <int M>
-struct ChainArgs {
-  int64_t Mrows;
-  int ns;             // number of leaves (all of width B)
-  Mat A, Y;
-  double* beta;
-  int64_t bps;
-  Mat Tall;           // leaf T's: leaf at column js at Tall.p + 32 js, ld 32
-  int* info;
-  int* leaf_done;     // [ns]
-  const int* apply_done;  // [ns]
-};
-
-__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_gpu(int* p, int v) {
-  asm volatile("st.release.gpu.global.b32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
-}
-
-template <int M, int B, int TPR, int NT>
-__global__ void __launch_bounds__(NT) leaf_chain_kernel(ChainArgs<M> c) {
-  const int C = (int)cg::this_cluster().num_blocks();
-  const int rank = (int)cg::this_cluster().block_rank();
-  for (int s = 0; s < c.ns; ++s) {
-    const int64_t js = (int64_t)s * B;
-    if (s >= 2) {
-      if (threadIdx.x == 0) {
-#ifdef MDLS_SPIN_DEBUG
-        long long it = 0;
-        while (ld_acquire_gpu(c.apply_done + s - 2) == 0 && ++it < 20000000) __nanosleep(64);
-        if (it >= 20000000) printf("leaf chain rank %d: stuck before leaf %d (apply_done[%d] = 0)\n", rank, s, s - 2);
-#else
-        while (ld_acquire_gpu(c.apply_done + s - 2) == 0) __nanosleep(64);
-#endif
-      }
-      __syncthreads();
-    }
-#ifdef MDLS_SPIN_DEBUG
-    if (rank == 0 && threadIdx.x == 0) printf("leaf %d start\n", s);
-#endif
-    const int64_t rows = c.Mrows - js;
-    const int64_t R = (rows + C - 1) / C;
-    LeafArgs<M> a;
-    a.Mrows = c.Mrows;
-    a.js = js;
-    a.R = R;
-    a.A = c.A;
-    a.Y = c.Y;
-    a.beta = c.beta;
-    a.bps = c.bps;
-    a.T.p = c.Tall.p + js * 32;
-    a.T.ld = 32;
-    a.T.ps = c.Tall.ps;
-    a.info = c.info;
-    a.Yp = c.Y;
-    a.Tp.p = c.Tall.p + (s > 0 ? (js - B) * 32 : 0);
-    a.Tp.ld = 32;
-    a.Tp.ps = c.Tall.ps;
-    a.jsp = s > 0 ? js - B : -1;
-    leaf_body<M, B, TPR, NT>(a, s == 0, s == 1, (uint32_t)((s - 1) & 1));
-    if (rank == 0 && threadIdx.x == 0) st_release_gpu(c.leaf_done + s, 1);
-  }
-}
-
 
 template <int M, int B, int TPR, int NT>
 cudaError_t leaf_reg_launch(cudaStream_t st, const LeafArgs<M>& la, int C) {
@@ -1125,22 +999,23 @@ cudaError_t leaf_reg_launch(cudaStream_t st, const LeafArgs<M>& la, int C) {
   // Exclusive SMs: request enough shared memory that no other CTA (the concurrent trailing / Q
   // GEMMs of the other streams) can share the leaf's SMs and their FP64 pipes -- the leaf is a
   // latency chain and would otherwise queue behind throughput-bound GEMM warps.  MDLS_LEAF_EXCL=0 off.
-  static size_t excl = 0;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static size_t excl_d[kMaxDev];  // kernel attributes are per device context
+  static bool attr_set[kMaxDev];
+  const int dev = cur_dev();
+  if (!attr_set[dev]) {
     const char* v = getenv("MDLS_LEAF_EXCL");
-    int optin = 0, dev = 0;
-    cudaGetDevice(&dev);
+    int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     cudaFuncAttributes fa{};
     cudaFuncGetAttributes(&fa, kern);
     const size_t room = (size_t)optin > fa.sharedSizeBytes ? (size_t)optin - fa.sharedSizeBytes : 0;
-    excl = (v && v[0] == '0') ? 0 : room;  // the whole opt-in shared memory: one leaf CTA per SM, alone
+    excl_d[dev] = (v && v[0] == '0') ? 0 : room;  // the whole opt-in shared memory: one leaf CTA per SM, alone
     cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)std::max(LeafPro<M, B, NT>::bytes, excl));
-    attr_set = true;
+                         (int)std::max(LeafPro<M, B, NT>::bytes, excl_d[dev]));
+    attr_set[dev] = true;
   }
+  const size_t excl = excl_d[dev];
   const size_t dyn = std::max((la.jsp >= 0) ? LeafPro<M, B, NT>::bytes : (size_t)0, excl);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(C, 1, 1);
@@ -1209,7 +1084,7 @@ inline size_t leaf_smem_bytes(int M, int B, int64_t R) { return sizeof(double) *
 template <int M>
 cudaError_t launch_leaf(cudaStream_t st, int64_t Mrows, int64_t js, int64_t bmax, Mat A, Mat Y, double* beta,
                         int64_t bps, Mat T, int* info, int* bw) {
-  static int csize = 16;
+  int csize = leaf_cluster_size();
   const int64_t rows = Mrows - js;
   const size_t cap = 200 * 1024;
   int B = 1;
@@ -1288,105 +1163,10 @@ cudaError_t launch_leaf_chain(cudaStream_t st, int64_t Mrows, int64_t js, int B,
   }
 }
 
-template <int M, int B, int TPR, int NT>
-cudaError_t leaf_chain_launch(cudaStream_t st, const ChainArgs<M>& ca, int C) {
-  auto kern = leaf_chain_kernel<M, B, TPR, NT>;
-  static size_t dyn = 0;
-  static bool attr_set = false;
-  if (!attr_set) {
-    int optin = 0, dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    cudaFuncAttributes fa{};
-    cudaFuncGetAttributes(&fa, kern);
-    const size_t room = (size_t)optin > fa.sharedSizeBytes ? (size_t)optin - fa.sharedSizeBytes : 0;
-    dyn = std::max(LeafPro<M, B, NT>::bytes, room);  // whole SMs for the duration of the factorisation
-    cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-    attr_set = true;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(C, 1, 1);
-  cfg.blockDim = dim3(NT, 1, 1);
-  cfg.dynamicSmemBytes = dyn;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = C;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  trace_begin(st, F_PANEL);
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ca);
-  trace_end(st, F_PANEL);
-  return e;
-}
-
-template <int M>
-cudaError_t launch_leaf_persistent(cudaStream_t st, int64_t Mrows, int ns, int B, Mat A, Mat Y, double* beta,
-                                   int64_t bps, Mat Tall, int* info, int* leaf_done, const int* apply_done) {
-  const int C = leaf_cluster_size();
-  const int64_t R = cdiv(Mrows, C);
-  ChainArgs<M> ca{Mrows, ns, A, Y, beta, bps, Tall, info, leaf_done, apply_done};
-  if constexpr (M == 2) {  // the persistent chain needs the prologue, used for dd only
-    if (R <= 64) return B == 16 ? leaf_chain_launch<M, 16, 4, 256>(st, ca, C) : leaf_chain_launch<M, 8, 4, 256>(st, ca, C);
-    return B == 16 ? leaf_chain_launch<M, 16, 4, 512>(st, ca, C) : leaf_chain_launch<M, 8, 4, 512>(st, ca, C);
-  } else {
-    (void)ca;
-    (void)R;
-    return cudaErrorNotSupported;
-  }
-}
-
-template <int M>
-cudaError_t launch_leaf_apply(cudaStream_t st, int64_t Mrows, int64_t jsl, int B, Mat A, Mat Y, Mat Tl, int64_t c0,
-                              int64_t c1) {
-  if (c1 <= c0) return cudaSuccess;
-  if constexpr (M != 2) {
-    return cudaErrorNotSupported;
-  } else {
-    constexpr int BB = 16, NT = 256;
-    if (B != BB) return cudaErrorNotSupported;
-    const int C = 16;
-    const int64_t rows = Mrows - (jsl + B);
-    if (rows <= 0) return cudaSuccess;
-    const int64_t R = cdiv(rows, C);
-    if (R > NT / 4) return cudaErrorNotSupported;
-    auto kern = leaf_apply_kernel<M, BB, 4, NT>;
-    static bool attr_set = false;
-    if (!attr_set) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LeafPro<M, BB, NT>::bytes);
-      attr_set = true;
-    }
-    LeafArgs<M> la{Mrows, jsl + B, R, A, Y, nullptr, 0, Tl, nullptr, Y, Tl, jsl};
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(C, (unsigned)cdiv(c1 - c0, B), 1);
-    cfg.blockDim = dim3(NT, 1, 1);
-    cfg.dynamicSmemBytes = LeafPro<M, BB, NT>::bytes;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = C;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    trace_begin(st, F_GEMM);
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, la, c0, c1);
-    trace_end(st, F_GEMM);
-    return e;
-  }
-}
-
 #define MDLS_INSTANTIATE_LEAF(MM)                                                                               \
   template cudaError_t launch_leaf<MM>(cudaStream_t, int64_t, int64_t, int64_t, Mat, Mat, double*, int64_t, Mat, \
                                        int*, int*);                                                                \
   template cudaError_t launch_leaf_chain<MM>(cudaStream_t, int64_t, int64_t, int, Mat, Mat, double*, int64_t, Mat, \
-                                             int*, Mat, int64_t);                                                    \
-  template cudaError_t launch_leaf_persistent<MM>(cudaStream_t, int64_t, int, int, Mat, Mat, double*, int64_t, Mat, \
-                                                  int*, int*, const int*);                                                   \
-  template cudaError_t launch_leaf_apply<MM>(cudaStream_t, int64_t, int64_t, int, Mat, Mat, Mat, int64_t, int64_t);
+                                             int*, Mat, int64_t);
 
 }  // namespace mdls

@@ -104,4 +104,35 @@ static __global__ void info_finish_kernel(const int* slot, const int* pre, int* 
 static __global__ void int_set_kernel(int* p, int v) { *p = v; }
 
 
+// ||y||_2 of an md vector of length n in md (f1: the least-squares residual norm from the trailing
+// entries of Q^T b): one CTA, per-thread accumulators over a fixed stride, a fixed-order
+// shared-memory tree of exact accumulator merges, one normalisation, md sqrt (QDlib-style, A0).
+template <int M>
+__global__ void __launch_bounds__(256) norm2_kernel(int64_t n, const double* __restrict__ y, int64_t psy,
+                                                    double* out, int64_t pso) {
+  __shared__ Acc<M> part[256];
+  Acc<M> acc;
+  acc.init();
+  int cnt = 0;
+  for (int64_t i = threadIdx.x; i < n; i += 256) {
+    const md<M> v = ld<M>(y, psy, i);
+    acc.add_prod(v, v);
+    if (++cnt == 8) {  // keep the lower bins small (md.cuh Acc)
+      acc.renorm_bins();
+      cnt = 0;
+    }
+  }
+  part[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = 128; s >= 1; s >>= 1) {
+    if ((int)threadIdx.x < s) {
+      Acc<M> a = part[threadIdx.x];
+      a.merge(part[threadIdx.x + s]);
+      part[threadIdx.x] = a;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) st<M>(out, pso, 0, sqrt<M>(part[0].get()));
+}
+
 }  // namespace mdls

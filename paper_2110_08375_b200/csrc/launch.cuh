@@ -12,12 +12,9 @@ template <int M, bool TA, bool TB>
 void gemm(cudaStream_t st, int64_t m, int64_t n, int64_t k, CMat A, CMat B, Mat C, int mode, double* part,
           int64_t part_cap_elems);
 
-template <int M, bool TA, bool TB>
-void gemm_preload();
 template <int M>
 void leaf_t_product(cudaStream_t st, int B, int64_t n, int64_t r, CMat Y, CMat T, CMat C, Mat X, double* part,
                     int64_t part_cap_elems);
-void flags_preload();  // ledger.cu
 
 template <int M>
 cudaError_t launch_leaf(cudaStream_t st, int64_t Mrows, int64_t js, int64_t bmax, Mat A, Mat Y, double* beta,
@@ -25,11 +22,11 @@ cudaError_t launch_leaf(cudaStream_t st, int64_t Mrows, int64_t js, int64_t bmax
 
 // chained leaves (register leaf with the previous-leaf prologue, kern_leaf.cuh)
 inline int leaf_cluster_size() {
-  static const int c = [] {
+  static const int force8 = [] {
     const char* v = getenv("MDLS_LEAF_C");
-    return (v && v[0] == '8') ? 8 : 16;
+    return (v && v[0] == '8') ? 1 : 0;
   }();
-  return c;
+  return force8 ? 8 : max_cluster_size();
 }
 template <int M>
 inline int chain_leaf_width(int64_t Mrows, int64_t js, int64_t bmax) {
@@ -46,15 +43,6 @@ inline int chain_leaf_width(int64_t Mrows, int64_t js, int64_t bmax) {
 template <int M>
 cudaError_t launch_leaf_chain(cudaStream_t st, int64_t Mrows, int64_t js, int B, Mat A, Mat Y, double* beta,
                               int64_t bps, Mat T, int* info, Mat Tp, int64_t jsp);
-
-template <int M>
-cudaError_t launch_leaf_persistent(cudaStream_t st, int64_t Mrows, int ns, int B, Mat A, Mat Y, double* beta,
-                                   int64_t bps, Mat Tall, int* info, int* leaf_done, const int* apply_done);
-template <int M>
-cudaError_t launch_leaf_apply(cudaStream_t st, int64_t Mrows, int64_t jsl, int B, Mat A, Mat Y, Mat Tl, int64_t c0,
-                              int64_t c1);
-void launch_wait_flag(cudaStream_t st, const int* f);  // kern_misc (ledger.cu TU)
-void launch_set_flag(cudaStream_t st, int* f);
 
 template <int M>
 void launch_invert(cudaStream_t st, int64_t ntiles, int64_t nb, CMat U, Mat Vt, double diag_scale, const double* dbeta,

@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "../../include/mdls.h"
+#include "types.cuh"
 
 // ---------------------------------------------------------------------------
 // launch accounting and per-stage tracing (declared in types.cuh)
@@ -101,34 +102,34 @@ void trace_end(cudaStream_t st, int family) {
   g_recs.push_back(Rec{t_stage, family, t_open, e1});
   t_open = nullptr;
 }
-// flags between the persistent leaf chain and the streams around it (solver.cuh::qr_factor_chain)
-__global__ void wait_flag_kernel(const int* f) {
-  if (threadIdx.x == 0) {
-    int v = 0;
-    do {
-      asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-      if (v == 0) __nanosleep(256);
-    } while (v == 0);
+// cluster-size probe: a 16-CTA cluster of whole-SM CTAs (the register leaf takes the opt-in shared
+// memory) needs the non-portable size; fall back to the portable 8 when the device cannot place it
+__global__ void cluster_probe_kernel() {}
+int max_cluster_size() {
+  static int c[kMaxDev] = {0};
+  const int d = cur_dev();
+  if (c[d] == 0) {
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, d);
+    cudaFuncSetAttribute(cluster_probe_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(cluster_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(16, 1, 1);
+    cfg.blockDim = dim3(256, 1, 1);
+    cfg.dynamicSmemBytes = (size_t)optin;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 16;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    const cudaError_t e = cudaOccupancyMaxActiveClusters(&n, cluster_probe_kernel, &cfg);
+    if (e != cudaSuccess) cudaGetLastError();
+    c[d] = (e == cudaSuccess && n >= 1) ? 16 : 8;
   }
-}
-__global__ void set_flag_kernel(int* f) {
-  __threadfence();
-  asm volatile("st.release.gpu.global.b32 [%0], %1;" :: "l"(f), "r"(1) : "memory");
-}
-void launch_wait_flag(cudaStream_t st, const int* f) {
-  trace_begin(st, 4 /* F_MISC */);
-  wait_flag_kernel<<<1, 32, 0, st>>>(f);
-  trace_end(st, 4 /* F_MISC */);
-}
-void flags_preload() {
-  cudaFuncAttributes fa{};
-  cudaFuncGetAttributes(&fa, wait_flag_kernel);
-  cudaFuncGetAttributes(&fa, set_flag_kernel);
-}
-void launch_set_flag(cudaStream_t st, int* f) {
-  trace_begin(st, 4 /* F_MISC */);
-  set_flag_kernel<<<1, 1, 0, st>>>(f);
-  trace_end(st, 4 /* F_MISC */);
+  return c[d];
 }
 
 }  // namespace mdls
@@ -143,7 +144,10 @@ constexpr T1 kT1[3] = {{20, 23, 70}, {89, 336, 893}, {269, 1742, 5126}};
 
 void count_house(int64_t n_j, mdls_counts* c) {
   // sigma: n-1 squares and sums; x1^2 + sigma; v1; beta = 2 v1^2 / (sigma + v1^2);
-  // 1/v1 and v = x * (1/v1)
+  // 1/v1 and v = x * (1/v1).  A column of length 1 (the last of a square matrix) has
+  // sigma = 0 (an empty sum): GVL Alg. 5.1.1 sets beta = 0 with no arithmetic.  The
+  // x1 > 0 branch is counted (v1 = -sigma / (x1 + mu): one division more than x1 <= 0).
+  if (n_j <= 1) return;
   c->mul[MDLS_ST_HOUSE] += (n_j - 1) + 1 + 2 + (n_j - 1);
   c->add[MDLS_ST_HOUSE] += (n_j - 1) + 1 + 1 + 1;
   c->div[MDLS_ST_HOUSE] += 3;
@@ -194,9 +198,10 @@ void count_qtb(int64_t M, int64_t K, int64_t nb, bool explicit_q, mdls_counts* c
 void count_bs(int64_t n, int64_t nb, mdls_counts* c) {
   const int64_t N = n / nb;
   // tile inversion exploiting zeros: column k (1-based) needs k(k-1)/2 pairs and
-  // k multiplications by the reciprocal diagonal; nb reciprocals per tile
+  // k-1 multiplications by the reciprocal diagonal (v_k = 1/u_kk itself is the
+  // reciprocal); nb reciprocals per tile
   const int64_t pairs = nb * (nb * nb - 1) / 6;
-  c->mul[MDLS_ST_INVERT] += N * (pairs + nb * (nb + 1) / 2);
+  c->mul[MDLS_ST_INVERT] += N * (pairs + nb * (nb - 1) / 2);
   c->add[MDLS_ST_INVERT] += N * pairs;
   c->div[MDLS_ST_INVERT] += N * nb;
   // x_i = U_i^-1 b_i: upper-triangular matvec

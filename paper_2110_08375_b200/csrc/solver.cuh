@@ -24,7 +24,7 @@ namespace mdls {
 // workspace plan (bytes, 256-aligned segments)
 // ---------------------------------------------------------------------------
 struct Plan {
-  size_t af = 0, q = 0, y = 0, w = 0, wl = 0, flags = 0, beta = 0, s = 0, t = 0, x = 0, part = 0, v0 = 0, v1 = 0, v2 = 0, vt = 0,
+  size_t af = 0, q = 0, y = 0, w = 0, beta = 0, s = 0, t = 0, x = 0, part = 0, v0 = 0, v1 = 0, v2 = 0, vt = 0,
          info = 0, total = 0;
 };
 
@@ -48,8 +48,6 @@ Plan make_plan(int op, int64_t Mr, int64_t K, int64_t nb) {
     p.beta = take(md * K);
     p.s = take(md * nb * nb);
     p.t = take(md * std::max<int64_t>(std::max<int64_t>(nb * nb, 1024), 32 * K));  // leaf T's (ld 32, column js)
-    p.wl = take(md * Mr * K);                                                       // leaf-local W_s = -Y_s T_s
-    p.flags = take(2 * sizeof(int) * (size_t)K);                                    // persistent-chain flags
   }
   if (op == MDLS_OP_APPLY_QT) p.y = take(md * Mr * K);
   if (qr_like || op == MDLS_OP_APPLY_QT) {
@@ -118,17 +116,19 @@ cudaError_t qr_panel(const Lane& L0, const Lane& L2, int64_t Mr, int64_t nb, int
     Mat Ws = sub(W, js, js);
     set_stage(MDLS_ST_WY);
     gemm<M, false, false>(L0.st, rs, bw, bw, Ys, cm(Tl), Ws, 3, nullptr, 0);  // W_s = -Y_s T_s
-    if (js > j0 && L2.st != L0.st) {
-      cudaEvent_t ev = pool_event();
-      cudaEventRecord(ev, L0.st);
-      cudaStreamWaitEvent(L2.st, ev, 0);
-    }
     const int64_t rem = j0 + nb - (js + bw);
     if (rem > 0) {
       set_stage(MDLS_ST_PANEL);
       Mat Cs = sub(A, js, js + bw);
       gemm<M, true, false>(L0.st, bw, rem, rs, cm(Ws), cm(Cs), L0.X, 0, L0.part, L0.cap);
       gemm<M, false, false>(L0.st, rs, rem, bw, Ys, cm(L0.X), Cs, 1, nullptr, 0);
+    }
+    // L2's recurrence below rewrites W(:, js:js+bw) (it adds W_< (Y_<^T W_s) into W_s), so it may only
+    // start once L0's in-panel product above has finished reading the leaf-local W_s
+    if (js > j0 && L2.st != L0.st) {
+      cudaEvent_t ev = pool_event();
+      cudaEventRecord(ev, L0.st);
+      cudaStreamWaitEvent(L2.st, ev, 0);
     }
     if (js > j0) {
       set_stage(MDLS_ST_WY);
@@ -187,10 +187,11 @@ cudaError_t qr_factor_overlap(const Lane& L0, const Lane& L1, const Lane& L2, in
   }
   const int64_t N = K / nb;
   cudaEvent_t trail_done = nullptr;  // L1: trailing update of the previous panel finished
+  cudaError_t e = cudaSuccess;
   for (int64_t k = 0; k < N; ++k) {
     const int64_t j0 = k * nb;
-    cudaError_t e = qr_panel<M>(L0, L2, Mr, nb, k, A, b.Y, b.W, b.beta, K, b);
-    if (e != cudaSuccess) return e;
+    e = qr_panel<M>(L0, L2, Mr, nb, k, A, b.Y, b.W, b.beta, K, b);
+    if (e != cudaSuccess) break;
     fork(L0.st, L2.st);  // W_k complete on L2 after this point
     cudaEvent_t wk = pool_event();
     cudaEventRecord(wk, L2.st);
@@ -206,9 +207,9 @@ cudaError_t qr_factor_overlap(const Lane& L0, const Lane& L1, const Lane& L2, in
     cudaEventRecord(trail_done, L1.st);
     if (Qf) form_q_forward_step<M>(L1, Mr, nb, k, *Qf, Yk, Wk);
   }
-  fork(L1.st, L0.st);
+  fork(L1.st, L0.st);  // joined even on an error (a caller's graph capture must not stay forked)
   fork(L2.st, L0.st);
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------
@@ -238,45 +239,15 @@ bool chain_supported(int64_t Mr, int64_t K, int64_t nb) {
 }
 
 template <int M>
-cudaError_t qr_factor_chain(cudaStream_t st, int64_t Mr, int64_t K, int64_t nb, Mat A, const QrBufs<M>& b, Mat Wl,
-                            Mat Tall, Mat* Qf, int* flags) {
-  // MDLS_PERSIST=1: persistent leaf chain (one cluster launch for all leaves, flags between the
-  // streams).  Off by default: it relies on concurrent kernel execution (it deadlocks when kernels
-  // are serialised, e.g. under a profiler's replay or CUDA_LAUNCH_BLOCKING=1).
-  // The previous-leaf prologue (in-cluster) applies leaf s-1 to leaf s's columns; MDLS_PROLOGUE=0
-  // applies it with GEMMs between the leaves instead (on the chain stream).
-  static const bool pro = [] {
-    const char* v = getenv("MDLS_PROLOGUE");
-    return v ? v[0] == '1' : true;  // measured: the GEMM variant is slower for qd/od too (39.8 vs 33.6 ms qd)
-  }();
-  static const bool persist = [] {
-    const char* v = getenv("MDLS_PERSIST");
-    return v && v[0] == '1';
-  }() && pro && M == 2;  // the persistent kernel is instantiated for dd only
+cudaError_t qr_factor_chain(cudaStream_t st, int64_t Mr, int64_t K, int64_t nb, Mat A, const QrBufs<M>& b, Mat Tall,
+                            Mat* Qf) {
   auto fork = [](cudaStream_t from, cudaStream_t to) {
     cudaEvent_t ev = pool_event();
     cudaEventRecord(ev, from);
     cudaStreamWaitEvent(to, ev, 0);
   };
-  static const bool q_high = [] {  // MDLS_Q_PRIO=high: forward Q on a high-priority stream
-    const char* v = getenv("MDLS_Q_PRIO");
-    return v && v[0] == 'h';
-  }();
-  cudaStream_t Lc = side_stream(0), Las = side_stream(1), Lws = side_stream(2), Lqs = side_stream(q_high ? 4 : 3);
+  cudaStream_t Lc = side_stream(0), Las = side_stream(1), Lws = side_stream(2), Lqs = side_stream(3);
   const Lane La = b.lane(0, Las), Lw = b.lane(1, Lws), Lq = b.lane(2, Lqs);
-  if (persist) {
-    static bool loaded = false;  // lazy module loading must not happen while the chain spins
-    if (!loaded) {
-      gemm_preload<M, false, false>();
-      gemm_preload<M, true, false>();
-      gemm_preload<M, false, true>();
-      flags_preload();
-      cudaFuncAttributes fa{};
-      cudaFuncGetAttributes(&fa, set_identity_kernel<M>);
-      loaded = true;
-    }
-    cudaMemsetAsync(flags, 0, 2 * sizeof(int) * (size_t)K, st);
-  }
   fork(st, Lc);
   fork(st, Las);
   fork(st, Lws);
@@ -295,14 +266,6 @@ cudaError_t qr_factor_chain(cudaStream_t st, int64_t Mr, int64_t K, int64_t nb, 
     js += B;
   }
   const int ns = (int)jss.size();
-  int* leaf_done = flags;
-  int* apply_done = flags + ns;
-  if (persist) {
-    set_stage(MDLS_ST_PANEL);
-    cudaError_t e = launch_leaf_persistent<M>(Lc, Mr, ns, Bs[0], A, b.Y, b.beta, K, Tall, b.info_slot, leaf_done,
-                                              apply_done);
-    if (e != cudaSuccess) return e;
-  }
   std::vector<cudaEvent_t> ev_apply((size_t)ns, nullptr);
   // MDLS_TIMELINE=1 (debug, not graph-capturable): per-leaf start/end and apply-end times, printed
   static const bool timeline = getenv("MDLS_TIMELINE") != nullptr;
@@ -315,78 +278,35 @@ cudaError_t qr_factor_chain(cudaStream_t st, int64_t Mr, int64_t K, int64_t nb, 
     return e;
   };
   if (timeline) tl0 = tl_ev(Lc);
-  for (int s = 0; s < ns; ++s) {
+  cudaError_t err = cudaSuccess;
+  for (int s = 0; s < ns && err == cudaSuccess; ++s) {
     const int64_t js = jss[(size_t)s];
     const int B = Bs[(size_t)s];
     const int64_t j0 = (js / nb) * nb, r = Mr - js;
     const Mat Ts{Tall.p + js * 32, 32, Tall.ps};
     cudaEvent_t ev_leaf = pool_event();
-    if (persist) {
-      set_stage(MDLS_ST_PANEL);
-      launch_wait_flag(Las, leaf_done + s);
-      cudaEventRecord(ev_leaf, Las);
-    } else {
-      if (s >= 2) cudaStreamWaitEvent(Lc, ev_apply[(size_t)s - 2], 0);
-      if (timeline) tl_ls.push_back(tl_ev(Lc));
-      set_stage(MDLS_ST_PANEL);
-      const Mat Tp = s > 0 ? Mat{Tall.p + jss[(size_t)s - 1] * 32, 32, Tall.ps} : Mat{nullptr, 0, 0};
-      cudaError_t e = launch_leaf_chain<M>(Lc, Mr, js, B, A, b.Y, b.beta, K, Ts, b.info_slot, Tp,
-                                           (pro && s > 0) ? jss[(size_t)s - 1] : -1);
-      if (e != cudaSuccess) return e;
-      if (!pro) {  // W_s = -Y_s T_s and leaf s applied to leaf s+1's columns, on the chain
-        const Lane Lcl = b.lane(3, Lc);
-        set_stage(MDLS_ST_WY);
-        gemm<M, false, false>(Lc, r, B, B, sub(cm(b.Y), js, js), cm(Ts), sub(Wl, js, js), 3, nullptr, 0);
-        if (s + 1 < ns) {
-          set_stage(MDLS_ST_PANEL);
-          // leaf s+1's columns must have leaf s-1 applied (La) before leaf s is applied here
-          if (s >= 1) cudaStreamWaitEvent(Lc, ev_apply[(size_t)s - 1], 0);
-          const int64_t jn = jss[(size_t)s + 1];
-          const int Bn = Bs[(size_t)s + 1];
-          const Mat Cn = sub(A, js, jn);
-          gemm<M, true, false>(Lc, B, Bn, r, sub(cm(Wl), js, js), cm(Cn), Lcl.X, 0, Lcl.part, Lcl.cap);
-          gemm<M, false, false>(Lc, r, Bn, B, sub(cm(b.Y), js, js), cm(Lcl.X), Cn, 1, nullptr, 0);
-        }
-      }
-      cudaEventRecord(ev_leaf, Lc);
-      if (timeline) tl_le.push_back(tl_ev(Lc));
-    }
-    // La: leaf W and the trailing update beyond leaf s+1
+    // Lc: leaf s (its prologue applies leaf s-1 to its own columns); leaf s-2 must have been applied to
+    // every column beyond leaf s-1 (La) first
+    if (s >= 2) cudaStreamWaitEvent(Lc, ev_apply[(size_t)s - 2], 0);
+    if (timeline) tl_ls.push_back(tl_ev(Lc));
+    set_stage(MDLS_ST_PANEL);
+    const Mat Tp = s > 0 ? Mat{Tall.p + jss[(size_t)s - 1] * 32, 32, Tall.ps} : Mat{nullptr, 0, 0};
+    err = launch_leaf_chain<M>(Lc, Mr, js, B, A, b.Y, b.beta, K, Ts, b.info_slot, Tp, s > 0 ? jss[(size_t)s - 1] : -1);
+    if (err != cudaSuccess) break;
+    cudaEventRecord(ev_leaf, Lc);
+    if (timeline) tl_le.push_back(tl_ev(Lc));
+    // La: the trailing update of leaf s beyond leaf s+1, C += Y_s X with X = -T_s^T (Y_s^T C) (the T
+    // product folded into the split-K reduction, so W_s is not needed on this stream)
     cudaStreamWaitEvent(Las, ev_leaf, 0);
     const CMat Ys = sub(cm(b.Y), js, js);
-    const Mat Wls = sub(Wl, js, js);
     const int64_t c0 = (s + 1 < ns) ? jss[(size_t)s + 1] + Bs[(size_t)s + 1] : K;
-    // dd: the whole trailing update of leaf s as one cluster launch (leaf_apply_kernel); else GEMMs
-    static const bool fused = [] {  // measured slower than the GEMMs (5.27 vs 4.97 ms dd without Q): opt-in
-      const char* v = getenv("MDLS_FUSED_APPLY");
-      return v && v[0] == '1';
-    }();
-    bool done = false;
-    if (fused && pro && c0 < K) {
-      set_stage(MDLS_ST_TRAILING);
-      done = launch_leaf_apply<M>(Las, Mr, js, B, A, b.Y, Ts, c0, K) == cudaSuccess;
-      if (!done) cudaGetLastError();
-    }
-    if (!done && pro && c0 < K && (B == 16 || B == 8)) {
-      // X = -T_s^T (Y_s^T C): no W_s on this stream (the T product is folded into the split-K reduction)
+    if (c0 < K) {
       set_stage(MDLS_ST_TRAILING);
       const Mat Cm = sub(A, js, c0);
       const Mat Xb{La.X.p, B, La.X.ps};
       leaf_t_product<M>(Las, B, K - c0, r, Ys, cm(Ts), cm(Cm), Xb, La.part, La.cap);
       gemm<M, false, false>(Las, r, K - c0, B, Ys, cm(Xb), Cm, 1, nullptr, 0);
-      done = true;
     }
-    if (!done) {
-      set_stage(MDLS_ST_WY);
-      if (pro) gemm<M, false, false>(Las, r, B, B, Ys, cm(Ts), Wls, 3, nullptr, 0);  // W_s = -Y_s T_s
-      if (c0 < K) {
-        set_stage(MDLS_ST_TRAILING);
-        const Mat Cm = sub(A, js, c0);
-        gemm<M, true, false>(Las, B, K - c0, r, cm(Wls), cm(Cm), La.X, 0, La.part, La.cap);
-        gemm<M, false, false>(Las, r, K - c0, B, Ys, cm(La.X), Cm, 1, nullptr, 0);
-      }
-    }
-    if (persist) launch_set_flag(Las, apply_done + s);
     ev_apply[(size_t)s] = pool_event();
     cudaEventRecord(ev_apply[(size_t)s], Las);
     if (timeline) tl_ae.push_back(tl_ev(Las));
@@ -405,10 +325,12 @@ cudaError_t qr_factor_chain(cudaStream_t st, int64_t Mr, int64_t K, int64_t nb, 
       form_q_forward_step<M>(Lq, Mr, nb, k, *Qf, sub(cm(b.Y), j0, j0), sub(cm(b.W), j0, j0));
     }
   }
+  // join every side stream even on an error, so a caller's graph capture is never left forked
   fork(Lc, st);
   fork(Las, st);
   fork(Lws, st);
   fork(Lqs, st);
+  if (err != cudaSuccess) return err;
   if (timeline) {
     cudaEvent_t tw = tl_ev(Lws), tq = tl_ev(Lqs);
     cudaDeviceSynchronize();

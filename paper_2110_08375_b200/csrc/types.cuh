@@ -49,15 +49,37 @@ struct CMat {
   int64_t ld, ps;
 };
 
-constexpr int kNumSMs = 148;
 constexpr int64_t kMaxSplit = 8;
+
+// per-device host state (kernel attributes, SM count, cluster support) is kept in
+// arrays indexed by the CUDA device ordinal: one process may drive several GPUs
+constexpr int kMaxDev = 64;
+inline int cur_dev() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return (d >= 0 && d < kMaxDev) ? d : 0;
+}
+// streaming multiprocessors of the current device (148 on B200)
+inline int num_sms() {
+  static int n[kMaxDev] = {0};
+  const int d = cur_dev();
+  if (n[d] <= 0) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d);
+    n[d] = v > 0 ? v : 148;
+  }
+  return n[d];
+}
+// largest thread-block cluster (16 non-portable, else 8) the current device can place with one
+// whole-SM CTA per cluster rank (probed once per device, ledger.cu)
+int max_cluster_size();
 
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 inline int grid_for(int64_t n, int threads) {
   int64_t g = cdiv(n, threads);
-  return (int)std::max<int64_t>(1, std::min<int64_t>(g, 8 * kNumSMs));
+  return (int)std::max<int64_t>(1, std::min<int64_t>(g, 8 * num_sms()));
 }
 
 

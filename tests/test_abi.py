@@ -16,9 +16,9 @@ HEADER = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))
 
 def declared_symbols():
     src = open(HEADER).read()
-    names = set(re.findall(r"\b(mdls_[a-z_]+)\s*\(", src.split("#define MDLS_DECLARE")[0]))
+    names = set(re.findall(r"\b(mdls_[a-z0-9_]+)\s*\(", src.split("#define MDLS_DECLARE")[0]))
     block = src.split("#define MDLS_DECLARE(P)")[1].split("MDLS_DECLARE(dd)")[0]
-    stems = set(re.findall(r"\b(mdls_[a-z_]+_)##P\s*\(", block))
+    stems = set(re.findall(r"\b(mdls_[a-z0-9_]+_)##P\s*\(", block))
     for p in ("dd", "qd", "od"):
         names |= {s + p for s in stems}
     return names

@@ -44,7 +44,6 @@ def test_md_ops_bitwise(orc, mdls, dev, prec, op):
     if op == "sqrt":
         a = np.where(a[0] < 0, -a, a)
     if op == "div":
-        b[:, 5] = a[:, 5] if False else b[:, 5]
         b = np.where(b[0] == 0, 1.0, b)
     ga, gb = torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev)
     got = mdls.md_op(op, prec, ga, None if op == "sqrt" else gb).cpu().numpy()
@@ -73,4 +72,5 @@ def test_fast_sqrt_recip_accuracy(orc, mdls, dev, prec):
         got = mdls.md_op(op, prec, ga).cpu().numpy()
         d = orc.md_op("sub", prec, got, ref)
         rel = np.abs(d[0]) / np.abs(ref[0])
+        print(f"{prec} {op}: max relative difference 2^({np.log2(max(np.max(rel), 1e-300)) + 53 * m:+.2f}) * 2^(-53m)")
         assert np.max(rel) <= 2.0 ** (-53 * m + 12), (op, np.max(rel))

@@ -102,3 +102,27 @@ def test_backsub_config4_full_sampled(orc, mdls, dev):
         scale = float(np.sum(np.abs(urow[0] * xs[0])))
         assert abs(r) <= 1e3 * n * u * scale, (i, r, scale)
     del U
+
+
+def test_backsub_config4_full_elementwise(orc, mdls, dev):
+    """BASELINE config 4 element by element: quad double, n = 17,920, tiles of 128 (the bench's
+    launch configuration) against the oracle's plain row back substitution of the same U and y
+    (about 1.6e8 qd pairs on the host).  Tolerance: north_star's 1e3 n u, scaled by max |x|."""
+    from ._parity import vec_ok
+
+    prec, n, nb = "qd", 17920, 128
+    U = inputs.lu_upper_torch(n, prec, seed=4, device=dev)
+    y = inputs.random_vector_torch(n, prec, seed=4, device=dev)
+    x, info = mdls.backsub(prec, U, y, nb)
+    torch.cuda.synchronize()
+    assert int(info.item()) == 0
+    xg = x.cpu().numpy()
+    yh = y.cpu().numpy()
+    Uh = U.cpu().numpy()
+    del U
+    torch.cuda.empty_cache()
+    xo, oinfo = orc.backsub(prec, Uh, yh)
+    assert oinfo == 0
+    err, tol = vec_ok(orc, prec, xg, xo, n)
+    print(f"config 4 elementwise: max |x_gpu - x_orc| = {err:.3e}, tol {tol:.3e} (ratio {err / tol:.2e})")
+    assert err <= tol
