@@ -26,14 +26,41 @@ __device__ __forceinline__ md<M> apply_mode(int mode, const md<M>& c, const md<M
   }
 }
 
+// asynchronous global -> shared copies (LDGSTS): 8-byte granules, so any double-aligned operand
+// (sub-matrix views with odd row offsets or odd leading dimensions included) can be staged; a
+// false predicate copies nothing and zero-fills the destination
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool pred) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s), "l"(gmem), "r"(pred ? 8 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// pipeline depth and padded shared-memory rows per precision (dynamic shared memory)
+template <int M, int V, bool TA, bool TB>
+struct GemmSmem {
+  using Tl = GemmTile<M, V>;
+  static constexpr int STAGES = (M == 8) ? 2 : 3;
+  // a +1 pad where the copy walks k fastest (transposed A, plain B): conflict-free scattered stores
+  static constexpr int BMP = Tl::BM + (TA ? 1 : 0);
+  static constexpr int BNP = Tl::BN + (TB ? 0 : 1);
+  static constexpr int A_ST = M * Tl::BK * BMP;  // doubles per stage
+  static constexpr int B_ST = M * Tl::BK * BNP;
+  static constexpr size_t bytes = sizeof(double) * (size_t)STAGES * (A_ST + B_ST);
+};
+
 template <int M, int V, bool TA, bool TB>
 __global__ void __launch_bounds__(GemmTile<M, V>::NT) gemm_kernel(GemmArgs g) {
   using Tl = GemmTile<M, V>;
+  using Sm = GemmSmem<M, V, TA, TB>;
   constexpr int BM = Tl::BM, BN = Tl::BN, BK = Tl::BK;
   constexpr int TM = Tl::TM, TN = Tl::TN;
   constexpr int NX = BN / TN, NY = BM / TM, NT = NX * NY;
-  __shared__ double As[M][BK][BM];
-  __shared__ double Bs[M][BK][BN];
+  constexpr int STAGES = Sm::STAGES, BMP = Sm::BMP, BNP = Sm::BNP;
+  extern __shared__ __align__(16) double gsm[];
+  double* As = gsm;                           // [STAGES][M][BK][BMP]
+  double* Bs = gsm + STAGES * Sm::A_ST;       // [STAGES][M][BK][BNP]
 
   const int tid = threadIdx.x;
   // consecutive lanes own consecutive output ROWS: the epilogue's C loads/stores and the split-K
@@ -42,6 +69,34 @@ __global__ void __launch_bounds__(GemmTile<M, V>::NT) gemm_kernel(GemmArgs g) {
   const int64_t i0 = (int64_t)blockIdx.y * BM, j0 = (int64_t)blockIdx.x * BN;
   const int64_t kb = (int64_t)blockIdx.z * g.kc;
   const int64_t ke = min(g.k, kb + g.kc);
+  const int nkt = (int)((ke - kb + BK - 1) / BK);
+
+  // issue the copies of k-tile t into stage t % STAGES (consecutive threads walk the contiguous
+  // direction of each operand: coalesced global reads)
+  auto load_tile = [&](int t) {
+    const int stg = t % STAGES;
+    const int64_t k0 = kb + (int64_t)t * BK;
+    double* as = As + stg * Sm::A_ST;
+    double* bs = Bs + stg * Sm::B_ST;
+    for (int e = tid; e < BM * BK; e += NT) {
+      int ii, kk;
+      if (TA) { kk = e % BK; ii = e / BK; } else { ii = e % BM; kk = e / BM; }
+      const int64_t gi = i0 + ii, gk = k0 + kk;
+      const bool ok = gi < g.m && gk < ke;
+      const int64_t off = ok ? (TA ? (gk + gi * g.lda) : (gi + gk * g.lda)) : 0;
+#pragma unroll
+      for (int l = 0; l < M; ++l) cp_async8(as + (l * BK + kk) * BMP + ii, g.A + l * g.psa + off, ok);
+    }
+    for (int e = tid; e < BK * BN; e += NT) {
+      int kk, jj;
+      if (TB) { jj = e % BN; kk = e / BN; } else { kk = e % BK; jj = e / BK; }
+      const int64_t gj = j0 + jj, gk = k0 + kk;
+      const bool ok = gj < g.n && gk < ke;
+      const int64_t off = ok ? (TB ? (gj + gk * g.ldb) : (gk + gj * g.ldb)) : 0;
+#pragma unroll
+      for (int l = 0; l < M; ++l) cp_async8(bs + (l * BK + kk) * BNP + jj, g.B + l * g.psb + off, ok);
+    }
+  };
 
   Acc<M> acc[TM][TN];
 #pragma unroll
@@ -49,50 +104,40 @@ __global__ void __launch_bounds__(GemmTile<M, V>::NT) gemm_kernel(GemmArgs g) {
 #pragma unroll
     for (int u = 0; u < TN; ++u) acc[t][u].init();
 
-  for (int64_t k0 = kb; k0 < ke; k0 += BK) {
-    // ---- stage A tile (BM x BK) ----
-    for (int e = tid; e < BM * BK; e += NT) {
-      int ii, kk;
-      if (TA) { kk = e % BK; ii = e / BK; } else { ii = e % BM; kk = e / BM; }
-      const int64_t gi = i0 + ii, gk = k0 + kk;
-      const bool ok = gi < g.m && gk < ke;
-      const int64_t off = TA ? (gk + gi * g.lda) : (gi + gk * g.lda);
 #pragma unroll
-      for (int l = 0; l < M; ++l) As[l][kk][ii] = ok ? g.A[l * g.psa + off] : 0.0;
-    }
-    // ---- stage B tile (BK x BN) ----
-    for (int e = tid; e < BK * BN; e += NT) {
-      int kk, jj;
-      if (TB) { jj = e % BN; kk = e / BN; } else { kk = e % BK; jj = e / BK; }
-      const int64_t gj = j0 + jj, gk = k0 + kk;
-      const bool ok = gj < g.n && gk < ke;
-      const int64_t off = TB ? (gj + gk * g.ldb) : (gk + gj * g.ldb);
-#pragma unroll
-      for (int l = 0; l < M; ++l) Bs[l][kk][jj] = ok ? g.B[l * g.psb + off] : 0.0;
-    }
-    __syncthreads();
+  for (int t = 0; t < STAGES - 1; ++t) {
+    if (t < nkt) load_tile(t);
+    cp_async_commit();  // one group per tile slot, empty past the end (keeps the wait counts uniform)
+  }
+  for (int t = 0; t < nkt; ++t) {
+    cp_async_wait<STAGES - 2>();  // this thread's copies of tile t have landed
+    __syncthreads();              // everyone's have; and everyone finished computing tile t-1
+    if (t + STAGES - 1 < nkt) load_tile(t + STAGES - 1);  // refill the stage tile t-1 used
+    cp_async_commit();
+    const double* as = As + (t % STAGES) * Sm::A_ST;
+    const double* bs = Bs + (t % STAGES) * Sm::B_ST;
 #pragma unroll 2
     for (int kk = 0; kk < BK; ++kk) {
       md<M> a[TM], b[TN];
 #pragma unroll
-      for (int t = 0; t < TM; ++t)
+      for (int i = 0; i < TM; ++i)
 #pragma unroll
-        for (int l = 0; l < M; ++l) a[t].v[l] = As[l][kk][ty + t * NY];
+        for (int l = 0; l < M; ++l) a[i].v[l] = as[(l * BK + kk) * BMP + ty + i * NY];
 #pragma unroll
       for (int u = 0; u < TN; ++u)
 #pragma unroll
-        for (int l = 0; l < M; ++l) b[u].v[l] = Bs[l][kk][tx + u * NX];
+        for (int l = 0; l < M; ++l) b[u].v[l] = bs[(l * BK + kk) * BNP + tx + u * NX];
 #pragma unroll
-      for (int t = 0; t < TM; ++t)
+      for (int i = 0; i < TM; ++i)
 #pragma unroll
-        for (int u = 0; u < TN; ++u) acc[t][u].add_prod(a[t], b[u]);
+        for (int u = 0; u < TN; ++u) acc[i][u].add_prod(a[i], b[u]);
     }
 #pragma unroll
-    for (int t = 0; t < TM; ++t)
+    for (int i = 0; i < TM; ++i)
 #pragma unroll
-      for (int u = 0; u < TN; ++u) acc[t][u].renorm_bins();
-    __syncthreads();
+      for (int u = 0; u < TN; ++u) acc[i][u].renorm_bins();
   }
+  cp_async_wait<0>();
 
   // ---- epilogue ----
 #pragma unroll
@@ -113,6 +158,38 @@ __global__ void __launch_bounds__(GemmTile<M, V>::NT) gemm_kernel(GemmArgs g) {
       }
     }
   }
+}
+
+// launch one gemm_kernel with its dynamic shared memory (attribute set once per device)
+template <int M, int V, bool TA, bool TB>
+void gemm_set_attr() {
+  using Sm = GemmSmem<M, V, TA, TB>;
+  static bool attr_set[kMaxDev];
+  const int dev = cur_dev();
+  if (!attr_set[dev]) {
+    cudaFuncSetAttribute(gemm_kernel<M, V, TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sm::bytes);
+    attr_set[dev] = true;
+  }
+}
+template <int M, int V, bool TA, bool TB>
+void gemm_kernel_launch(cudaStream_t st, dim3 grid, const GemmArgs& g) {
+  gemm_set_attr<M, V, TA, TB>();
+  MDLS_LAUNCH(F_GEMM, st,
+              gemm_kernel<M, V, TA, TB><<<grid, GemmTile<M, V>::NT, GemmSmem<M, V, TA, TB>::bytes, st>>>(g));
+}
+// resident CTAs of this variant on the whole device (occupancy x SMs), once per device
+template <int M, int V, bool TA, bool TB>
+int64_t gemm_slots() {
+  static int64_t slots[kMaxDev];
+  const int dev = cur_dev();
+  if (slots[dev] <= 0) {
+    gemm_set_attr<M, V, TA, TB>();
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gemm_kernel<M, V, TA, TB>, GemmTile<M, V>::NT,
+                                                  GemmSmem<M, V, TA, TB>::bytes);
+    slots[dev] = (int64_t)std::max(1, per_sm) * num_sms();
+  }
+  return slots[dev];
 }
 
 // C (mode)= sum_{z=0..S-1} part_z, in split order
@@ -153,19 +230,30 @@ void gemm_launch(cudaStream_t st, int64_t m, int64_t n, int64_t k, CMat A, CMat 
                  int64_t part_cap_elems) {
   using Tl = GemmTile<M, V>;
   const int64_t tiles = cdiv(m, Tl::BM) * cdiv(n, Tl::BN);
-  const int64_t target = 2 * num_sms();
+  // split-K: choose the split that minimises (waves of resident CTAs) x (k-tiles per CTA) plus the
+  // partial round trip (written by the GEMM, read by the fixed-order reduction: ~0.3 (S + 2) k-tile
+  // waves of the tiles' share of the device)
+  const int64_t slots = gemm_slots<M, V, TA, TB>();
+  const int64_t kt = cdiv(k, Tl::BK);
   int64_t S = 1;
-  if (part && tiles < target && k >= 4 * Tl::BK) {
-    S = std::min<int64_t>(kMaxSplitK, cdiv(target, tiles));
-    S = std::min<int64_t>(S, k / (2 * Tl::BK));
-    while (S > 1 && m * n * S > part_cap_elems) --S;
-    S = std::max<int64_t>(S, 1);
+  if (part && kt >= 4) {
+    double best = 1e300;
+    for (int64_t s = 1; s <= std::min<int64_t>(kMaxSplitK, kt / 2); ++s) {
+      const int64_t per = cdiv(kt, s), se = cdiv(kt, per);
+      if (se > 1 && m * n * se > part_cap_elems) break;
+      const double cost = (double)(cdiv(tiles * se, slots) * per) +
+                          (se > 1 ? 0.3 * (double)(se + 2) * (double)tiles / (double)slots : 0.0);
+      if (cost < best - 1e-9) {
+        best = cost;
+        S = se;
+      }
+    }
   }
   int64_t kc = cdiv(cdiv(k, S), Tl::BK) * Tl::BK;
   S = std::max<int64_t>(1, cdiv(k, kc));
   GemmArgs g{m, n, k, A.p, A.ld, A.ps, B.p, B.ld, B.ps, C.p, C.ld, C.ps, mode, kc, S > 1 ? part : nullptr, S};
   dim3 grid((unsigned)cdiv(n, Tl::BN), (unsigned)cdiv(m, Tl::BM), (unsigned)S);
-  MDLS_LAUNCH(F_GEMM, st, gemm_kernel<M, V, TA, TB><<<grid, Tl::NT, 0, st>>>(g));
+  gemm_kernel_launch<M, V, TA, TB>(st, grid, g);
   if (S > 1)
     MDLS_LAUNCH(F_GEMM, st, splitk_reduce_kernel<M><<<grid_for(m * n, 256), 256, 0, st>>>(m, n, S, part, C.p, C.ld, C.ps, mode));
 }
@@ -239,7 +327,7 @@ void leaf_t_product(cudaStream_t st, int B, int64_t n, int64_t r, CMat Y, CMat T
   S = std::max<int64_t>(1, cdiv(r, kc));
   GemmArgs g{B, n, r, Y.p, Y.ld, Y.ps, C.p, C.ld, C.ps, nullptr, B, 0, 0, kc, part, S};
   dim3 grid((unsigned)cdiv(n, Tl::BN), (unsigned)cdiv(B, Tl::BM), (unsigned)S);
-  MDLS_LAUNCH(F_GEMM, st, gemm_kernel<M, 2, true, false><<<grid, Tl::NT, 0, st>>>(g));
+  gemm_kernel_launch<M, 2, true, false>(st, grid, g);
   if (B == 16)
     MDLS_LAUNCH(F_GEMM, st, splitk_reduce_t_kernel<M, 16><<<(unsigned)cdiv(n, 16), 256, 0, st>>>(n, S, part, T, X.p, X.ld, X.ps));
   else
