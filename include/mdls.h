@@ -173,6 +173,20 @@ int mdls_trace_collect(double *stage_ms, double *family_ms, int64_t *family_laun
                      double *Q_out, int64_t ldq, int64_t psq, double *y_out, int64_t psy, void *work,              \
                      size_t work_bytes, int *dev_info, void *stream);                                              \
                                                                                                                    \
+  /* a batch of independent least-squares problems (SURVEY 8e batch sharding; the paper's motivation is many     \
+   * solves inside a path tracker): problem p = 0..batch-1 is mdls_lstsq on A + p*strideA,             \
+   * b + p*strideB, x + p*strideX (strides in doubles, no overlap: strideA >= (m-1)*psa + lda*K etc.), all of     \
+   * the same M x K shape and tile nb.  The problems run on `groups` (1..16) library stream groups -- problem p on \
+   * group p mod groups with the workspace slice p mod groups -- so up to `groups` solves overlap on the device; \
+   * every group is forked from and joined into `stream`.  work: mdls_workspace_batched_<p>(op, M, K, nb, groups)\
+   * bytes.  dev_info (nullable): batch device ints, entry p as mdls_lstsq's dev_info of problem p. */           \
+  int mdls_lstsq_batched_##P(int64_t batch, int64_t M, int64_t K, int64_t nb, const double *A, int64_t lda,        \
+                             int64_t psa, int64_t strideA, const double *b, int64_t psb, int64_t strideB,          \
+                             double *x, int64_t psx, int64_t strideX, int form_q, int groups, void *work,          \
+                             size_t work_bytes, int *dev_info, void *stream);                                      \
+  /* bytes of `work` for mdls_lstsq_batched_<p> (op MDLS_OP_LSTSQ or MDLS_OP_LSTSQ_NOQ); 0 for invalid sizes. */ \
+  size_t mdls_workspace_batched_##P(int op, int64_t M, int64_t K, int64_t nb, int groups);                        \
+                                                                                                                   \
   /* ||y||_2 of the md vector y of length n (n >= 0), in md: one md number written to out (limb l at           \
    * out[l*pso]).  With y = (Q^T b)(K+1:M) from mdls_lstsq's y_out this is the least-squares residual norm        \
    * ||b - A x||_2 (orthogonality of Q).  Fixed-order reduction (bitwise reproducible). */  \

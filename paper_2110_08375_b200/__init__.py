@@ -231,6 +231,38 @@ def lstsq(prec: str, A, b, nb: int, form_q: bool = True, want_R: bool = False, w
     return LstsqResult(x, R, Q, y if want_y else None, info, res)
 
 
+def batch_workspace_bytes(prec: str, op: int, M: int, K: int, nb: int, groups: int) -> int:
+    return int(_lib.fn("mdls_workspace_batched_", prec)(op, M, K, nb, groups))
+
+
+def lstsq_batched(prec: str, A, b, nb: int, form_q: bool = True, groups: int = 4, work=None):
+    """Independent least-squares problems (mdls_lstsq_batched_<p>): A (B, m, K, M), b (B, m, M) -> x (B, m, K),
+    info (B,).  Problem p runs on stream group p mod ``groups``; up to ``groups`` solves overlap."""
+    torch = _torch()
+    if A.dim() != 4 or b.dim() != 3:
+        raise ValueError("A must be (B, m, K, M) and b (B, m, M)")
+    Bn, m, K, M = A.shape
+    _check_md(A[0], prec, 3, "A")
+    _check_md(b[0], prec, 2, "b")
+    if not (A.is_contiguous() and b.is_contiguous()):
+        raise ValueError("A and b must be contiguous")
+    dev = A.device
+    x = torch.empty((Bn, m, K), dtype=torch.float64, device=dev)
+    info = torch.zeros(max(Bn, 1), dtype=torch.int32, device=dev)
+    op = _lib.OP_LSTSQ if form_q else _lib.OP_LSTSQ_NOQ
+    groups = max(1, min(int(groups), 16))
+    nbytes = batch_workspace_bytes(prec, op, M, K, nb, groups)
+    if nbytes == 0:
+        raise ValueError("invalid batched least-squares shape")
+    if work is None or work.numel() < nbytes:
+        work = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    rc = _lib.fn("mdls_lstsq_batched_", prec)(Bn, M, K, nb, _ptr(A), M, K * M, m * K * M, _ptr(b), M, m * M,
+                                              _ptr(x), K, m * K, int(form_q), groups, _ptr(work), work.numel(),
+                                              _ptr(info), _stream())
+    _lib.check(rc, "lstsq_batched")
+    return x, info[:Bn]
+
+
 def launch_count() -> int:
     """Kernels launched by libmdls since load (host counter)."""
     return int(_lib.load().mdls_launch_count())

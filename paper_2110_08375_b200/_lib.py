@@ -49,6 +49,8 @@ _SIGS = {
     "mdls_lstsq_": (_I, [_L, _L, _L, _P, _L, _L, _P, _L, _P, _L, _I, _P, _L, _L, _P, _L, _L, _P, _L, _P, _Z, _P,
                          _P]),
     "mdls_norm2_": (_I, [_L, _P, _L, _P, _L, _P]),
+    "mdls_lstsq_batched_": (_I, [_L, _L, _L, _L, _P, _L, _L, _L, _P, _L, _L, _P, _L, _L, _I, _I, _P, _Z, _P, _P]),
+    "mdls_workspace_batched_": (_Z, [_I, _L, _L, _L, _I]),
     "mdls_qr_panel_": (_I, [_L, _L, _L, _P, _L, _L, _P, _L, _L, _P, _L, _L, _P, _Z, _P, _P]),
     "mdls_qr_update_": (_I, [_L, _L, _L, _P, _L, _L, _P, _L, _L, _P, _L, _L, _L, _L, _P, _Z, _P]),
 }

@@ -151,6 +151,54 @@ static QrBufs<M> qr_bufs(void* work, const Plan& p, int64_t Mr, int64_t K, int64
   return b;
 }
 
+// the whole least-squares pipeline of one problem on stream st (arguments already checked)
+static int lstsq_run(cudaStream_t st, int64_t Mr, int64_t K, int64_t nb, const double* A, int64_t lda, int64_t psa,
+                     const double* b, int64_t psb, double* x, int64_t psx, int form_q, double* R_out, int64_t ldr,
+                     int64_t psr, double* Q_out, int64_t ldq, int64_t psq, double* y_out, int64_t psy, void* work,
+                     int* dev_info) {
+  const int op = form_q ? MDLS_OP_LSTSQ : MDLS_OP_LSTSQ_NOQ;
+  const Plan p = make_plan<M>(op, Mr, K, nb);
+  set_stage(MDLS_NSTAGES);
+  QrBufs<M> bb = qr_bufs(work, p, Mr, K, nb, nullptr, 0, 0);
+  int* pre = bb.info_slot + 2;
+  MDLS_LAUNCH(F_MISC, st, info_init_kernel<<<1, 1, 0, st>>>(bb.info_slot));
+  MDLS_LAUNCH(F_MISC, st, info_init_kernel<<<1, 1, 0, st>>>(bb.info_slot + 1));
+  MDLS_LAUNCH(F_MISC, st, int_set_kernel<<<1, 1, 0, st>>>(pre, 0));
+  MDLS_LAUNCH(F_MISC, st, finite_check_kernel<M><<<grid_for(Mr * K, 256), 256, 0, st>>>(Mr, K, CMat{A, lda, psa}, pre));
+  MDLS_LAUNCH(F_MISC, st, finite_check_kernel<M><<<grid_for(Mr, 256), 256, 0, st>>>(Mr, 1, CMat{b, Mr, psb}, pre));
+  // factor a copy of A
+  Mat Af{at<double>(work, p.af), Mr, Mr * K};
+  MDLS_LAUNCH(F_MISC, st, copy_kernel<M><<<grid_for(Mr * K, 256), 256, 0, st>>>(Mr, K, CMat{A, lda, psa}, Af, 0));
+  cudaMemsetAsync(bb.Y.p, 0, sizeof(double) * M * Mr * K, st);
+  cudaMemsetAsync(bb.W.p, 0, sizeof(double) * M * Mr * K, st);
+  Mat Q = (form_q && Q_out) ? Mat{Q_out, ldq, psq} : Mat{form_q ? at<double>(work, p.q) : nullptr, Mr, Mr * Mr};
+  const bool fwd = form_q && q_forward<M>();
+  if (use_chain<M>(Mr, K, nb)) {
+    if (qr_factor_chain<M>(st, Mr, K, nb, Af, bb, Mat{at<double>(work, p.t), 32, 32 * std::max<int64_t>(K, 32)},
+                           fwd ? &Q : nullptr) != cudaSuccess)
+      return MDLS_ERR_CUDA;
+  } else if (qr_factor_overlap<M>(bb.lane(0, st), bb.lane(1, side_stream(0)), bb.lane(2, side_stream(1)), Mr, K, nb,
+                                  Af, bb, fwd ? &Q : nullptr) != cudaSuccess) {
+    return MDLS_ERR_CUDA;
+  }
+  double* yv = at<double>(work, p.v1);
+  if (form_q) {
+    if (!fwd) form_q_backward<M>(st, Mr, K, nb, Q, bb);
+    set_stage(MDLS_ST_QTB);
+    gemm<M, true, false>(st, Mr, 1, Mr, cm(Q), CMat{b, Mr, psb}, Mat{yv, Mr, Mr}, 0, bb.part, bb.part_cap);
+  } else {
+    MDLS_LAUNCH(F_MISC, st, copy_kernel<M><<<grid_for(Mr, 256), 256, 0, st>>>(Mr, 1, CMat{b, Mr, psb}, Mat{yv, Mr, Mr}, 0));
+    apply_qt_panels<M>(st, Mr, K, nb, cm(bb.Y), cm(bb.W), Mat{yv, Mr, Mr}, bb.X, bb.part, bb.part_cap);
+  }
+  backsub<M>(st, K, nb, cm(Af), yv, Mr, x, psx, Mat{at<double>(work, p.vt), nb, nb * K}, at<double>(work, p.v0),
+             bb.info_slot);
+  set_stage(MDLS_NSTAGES);
+  if (R_out) MDLS_LAUNCH(F_MISC, st, copy_kernel<M><<<grid_for(Mr * K, 256), 256, 0, st>>>(Mr, K, cm(Af), Mat{R_out, ldr, psr}, 1));
+  if (y_out) MDLS_LAUNCH(F_MISC, st, copy_kernel<M><<<grid_for(Mr, 256), 256, 0, st>>>(Mr, 1, CMat{yv, Mr, Mr}, Mat{y_out, Mr, psy}, 0));
+  if (dev_info) MDLS_LAUNCH(F_MISC, st, info_finish_kernel<<<1, 1, 0, st>>>(bb.info_slot, pre, dev_info));
+  return launched();
+}
+
 int MDLS_FN(mdls_qr_)(int64_t Mr, int64_t K, int64_t nb, double* A, int64_t lda, int64_t psa, double* Q, int64_t ldq,
                       int64_t psq, double* W, int64_t ldw, int64_t psw, void* work, size_t work_bytes, int* dev_info,
                       void* stream) {
@@ -282,48 +330,60 @@ int MDLS_FN(mdls_lstsq_)(int64_t Mr, int64_t K, int64_t nb, const double* A, int
   if (Q_out && !mat_ok(Q_out, Mr, Mr, ldq, psq)) return -15;
   if (y_out && psy < Mr) return -19;
   const int op = form_q ? MDLS_OP_LSTSQ : MDLS_OP_LSTSQ_NOQ;
-  const Plan p = make_plan<M>(op, Mr, K, nb);
-  if (!work || work_bytes < p.total) return -21;
+  if (!work || work_bytes < make_plan<M>(op, Mr, K, nb).total) return -21;
+  return lstsq_run(S(stream), Mr, K, nb, A, lda, psa, b, psb, x, psx, form_q, R_out, ldr, psr, Q_out, ldq, psq, y_out,
+                   psy, work, dev_info);
+}
+
+// independent least-squares problems p = 0..batch-1 (A_p = A + p*strideA, b_p, x_p likewise):
+// problem p runs on stream group p mod G with workspace slice p mod G, so G solves overlap on the device
+int MDLS_FN(mdls_lstsq_batched_)(int64_t batch, int64_t Mr, int64_t K, int64_t nb, const double* A, int64_t lda,
+                                 int64_t psa, int64_t strideA, const double* b, int64_t psb, int64_t strideB,
+                                 double* x, int64_t psx, int64_t strideX, int form_q, int groups, void* work,
+                                 size_t work_bytes, int* dev_info, void* stream) {
+  if (batch < 0) return -1;
+  if (int e = tile_ok(Mr, K, nb)) return e - 1;
+  if (!mat_ok(A, Mr, K, lda, psa)) return -5;
+  if (strideA < (M - 1) * psa + lda * K) return -8;
+  if (!b || psb < Mr) return -9;
+  if (strideB < (M - 1) * psb + Mr) return -11;
+  if (!x || psx < K) return -12;
+  if (strideX < (M - 1) * psx + K) return -14;
+  if (groups < 1 || groups > kMaxGroups) return -16;
+  const int op = form_q ? MDLS_OP_LSTSQ : MDLS_OP_LSTSQ_NOQ;
+  const size_t slice = align256(make_plan<M>(op, Mr, K, nb).total);
+  if (!work || work_bytes < slice * (size_t)groups) return -18;
+  if (batch == 0) return 0;
   cudaStream_t st = S(stream);
-  set_stage(MDLS_NSTAGES);
-  QrBufs<M> bb = qr_bufs(work, p, Mr, K, nb, nullptr, 0, 0);
-  int* pre = bb.info_slot + 2;
-  MDLS_LAUNCH(F_MISC, st, info_init_kernel<<<1, 1, 0, st>>>(bb.info_slot));
-  MDLS_LAUNCH(F_MISC, st, info_init_kernel<<<1, 1, 0, st>>>(bb.info_slot + 1));
-  MDLS_LAUNCH(F_MISC, st, int_set_kernel<<<1, 1, 0, st>>>(pre, 0));
-  MDLS_LAUNCH(F_MISC, st, finite_check_kernel<M><<<grid_for(Mr * K, 256), 256, 0, st>>>(Mr, K, CMat{A, lda, psa}, pre));
-  MDLS_LAUNCH(F_MISC, st, finite_check_kernel<M><<<grid_for(Mr, 256), 256, 0, st>>>(Mr, 1, CMat{b, Mr, psb}, pre));
-  // factor a copy of A
-  Mat Af{at<double>(work, p.af), Mr, Mr * K};
-  MDLS_LAUNCH(F_MISC, st, copy_kernel<M><<<grid_for(Mr * K, 256), 256, 0, st>>>(Mr, K, CMat{A, lda, psa}, Af, 0));
-  cudaMemsetAsync(bb.Y.p, 0, sizeof(double) * M * Mr * K, st);
-  cudaMemsetAsync(bb.W.p, 0, sizeof(double) * M * Mr * K, st);
-  Mat Q = (form_q && Q_out) ? Mat{Q_out, ldq, psq} : Mat{form_q ? at<double>(work, p.q) : nullptr, Mr, Mr * Mr};
-  const bool fwd = form_q && q_forward<M>();
-  if (use_chain<M>(Mr, K, nb)) {
-    if (qr_factor_chain<M>(st, Mr, K, nb, Af, bb, Mat{at<double>(work, p.t), 32, 32 * std::max<int64_t>(K, 32)},
-                           fwd ? &Q : nullptr) != cudaSuccess)
-      return MDLS_ERR_CUDA;
-  } else if (qr_factor_overlap<M>(bb.lane(0, st), bb.lane(1, side_stream(0)), bb.lane(2, side_stream(1)), Mr, K, nb,
-                                  Af, bb, fwd ? &Q : nullptr) != cudaSuccess) {
-    return MDLS_ERR_CUDA;
+  const int G = (int)std::min<int64_t>(groups, batch);
+  std::vector<cudaStream_t> gst((size_t)G);
+  for (int g = 0; g < G; ++g) {
+    StreamGroup sg(g);
+    gst[(size_t)g] = side_stream(6);
+    cudaEvent_t ev = pool_event();
+    cudaEventRecord(ev, st);
+    cudaStreamWaitEvent(gst[(size_t)g], ev, 0);
   }
-  double* yv = at<double>(work, p.v1);
-  if (form_q) {
-    if (!fwd) form_q_backward<M>(st, Mr, K, nb, Q, bb);
-    set_stage(MDLS_ST_QTB);
-    gemm<M, true, false>(st, Mr, 1, Mr, cm(Q), CMat{b, Mr, psb}, Mat{yv, Mr, Mr}, 0, bb.part, bb.part_cap);
-  } else {
-    MDLS_LAUNCH(F_MISC, st, copy_kernel<M><<<grid_for(Mr, 256), 256, 0, st>>>(Mr, 1, CMat{b, Mr, psb}, Mat{yv, Mr, Mr}, 0));
-    apply_qt_panels<M>(st, Mr, K, nb, cm(bb.Y), cm(bb.W), Mat{yv, Mr, Mr}, bb.X, bb.part, bb.part_cap);
+  int rc = 0;
+  for (int64_t p = 0; p < batch && rc == 0; ++p) {
+    const int g = (int)(p % G);
+    StreamGroup sg(g);
+    rc = lstsq_run(gst[(size_t)g], Mr, K, nb, A + p * strideA, lda, psa, b + p * strideB, psb, x + p * strideX, psx,
+                   form_q, nullptr, 0, 0, nullptr, 0, 0, nullptr, 0, static_cast<char*>(work) + slice * (size_t)g,
+                   dev_info ? dev_info + p : nullptr);
   }
-  backsub<M>(st, K, nb, cm(Af), yv, Mr, x, psx, Mat{at<double>(work, p.vt), nb, nb * K}, at<double>(work, p.v0),
-             bb.info_slot);
-  set_stage(MDLS_NSTAGES);
-  if (R_out) MDLS_LAUNCH(F_MISC, st, copy_kernel<M><<<grid_for(Mr * K, 256), 256, 0, st>>>(Mr, K, cm(Af), Mat{R_out, ldr, psr}, 1));
-  if (y_out) MDLS_LAUNCH(F_MISC, st, copy_kernel<M><<<grid_for(Mr, 256), 256, 0, st>>>(Mr, 1, CMat{yv, Mr, Mr}, Mat{y_out, Mr, psy}, 0));
-  if (dev_info) MDLS_LAUNCH(F_MISC, st, info_finish_kernel<<<1, 1, 0, st>>>(bb.info_slot, pre, dev_info));
-  return launched();
+  for (int g = 0; g < G; ++g) {  // joined even on an error (a caller's graph capture must not stay forked)
+    cudaEvent_t ev = pool_event();
+    cudaEventRecord(ev, gst[(size_t)g]);
+    cudaStreamWaitEvent(st, ev, 0);
+  }
+  return rc;
+}
+
+size_t MDLS_FN(mdls_workspace_batched_)(int op, int64_t Mr, int64_t K, int64_t nb, int groups) {
+  if (op != MDLS_OP_LSTSQ && op != MDLS_OP_LSTSQ_NOQ) return 0;
+  if (groups < 1 || groups > kMaxGroups || tile_ok(Mr, K, nb)) return 0;
+  return align256(make_plan<M>(op, Mr, K, nb).total) * (size_t)groups;
 }
 
 int MDLS_FN(mdls_qr_panel_)(int64_t Mr, int64_t nb, int64_t k, double* Ak, int64_t lda, int64_t psa, double* Wk,

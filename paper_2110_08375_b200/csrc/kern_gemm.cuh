@@ -66,8 +66,14 @@ __global__ void __launch_bounds__(GemmTile<M, V>::NT) gemm_kernel(GemmArgs g) {
   // consecutive lanes own consecutive output ROWS: the epilogue's C loads/stores and the split-K
   // partial stores are coalesced along the column-major planes (they dominate when k is small)
   const int ty = tid % NY, tx = tid / NY;
-  const int64_t i0 = (int64_t)blockIdx.y * BM, j0 = (int64_t)blockIdx.x * BN;
-  const int64_t kb = (int64_t)blockIdx.z * g.kc;
+  // work items (column tile fastest, then row tile, then split) in a grid-stride loop: one item per
+  // CTA normally; a capped grid (GemmCap) keeps a low-priority product to part of the device
+  const int64_t ntx = (g.n + BN - 1) / BN, nty = (g.m + BM - 1) / BM;
+  const int64_t nitems = ntx * nty * g.S;
+  for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
+  const int64_t z = item / (ntx * nty);
+  const int64_t i0 = ((item / ntx) % nty) * BM, j0 = (item % ntx) * BN;
+  const int64_t kb = z * g.kc;
   const int64_t ke = min(g.k, kb + g.kc);
   const int nkt = (int)((ke - kb + BK - 1) / BK);
 
@@ -150,13 +156,15 @@ __global__ void __launch_bounds__(GemmTile<M, V>::NT) gemm_kernel(GemmArgs g) {
       if (gj >= g.n) continue;
       if (g.part) {
         const int64_t pps = g.m * g.n * g.S;
-        st<M>(g.part, pps, gi + (gj + blockIdx.z * g.n) * g.m, acc[t][u].get());
+        st<M>(g.part, pps, gi + (gj + z * g.n) * g.m, acc[t][u].get());
       } else {
         const int64_t e = gi + gj * g.ldc;
         md<M> c = (g.mode == 1 || g.mode == 2) ? ld<M>(g.C, g.psc, e) : md_zero<M>();
         st<M>(g.C, g.psc, e, apply_mode<M>(g.mode, c, acc[t][u].get()));
       }
     }
+  }
+  if (item + gridDim.x < nitems) __syncthreads();  // every thread done with the stages before the refill
   }
 }
 
@@ -172,10 +180,14 @@ void gemm_set_attr() {
   }
 }
 template <int M, int V, bool TA, bool TB>
-void gemm_kernel_launch(cudaStream_t st, dim3 grid, const GemmArgs& g) {
+void gemm_kernel_launch(cudaStream_t st, const GemmArgs& g) {
+  using Tl = GemmTile<M, V>;
   gemm_set_attr<M, V, TA, TB>();
+  int64_t items = cdiv(g.m, Tl::BM) * cdiv(g.n, Tl::BN) * g.S;
+  if (g_gemm_cta_cap > 0) items = std::min<int64_t>(items, g_gemm_cta_cap);
+  const dim3 grid((unsigned)std::max<int64_t>(1, items));
   MDLS_LAUNCH(F_GEMM, st,
-              gemm_kernel<M, V, TA, TB><<<grid, GemmTile<M, V>::NT, GemmSmem<M, V, TA, TB>::bytes, st>>>(g));
+              gemm_kernel<M, V, TA, TB><<<grid, Tl::NT, GemmSmem<M, V, TA, TB>::bytes, st>>>(g));
 }
 // resident CTAs of this variant on the whole device (occupancy x SMs), once per device
 template <int M, int V, bool TA, bool TB>
@@ -233,7 +245,8 @@ void gemm_launch(cudaStream_t st, int64_t m, int64_t n, int64_t k, CMat A, CMat 
   // split-K: choose the split that minimises (waves of resident CTAs) x (k-tiles per CTA) plus the
   // partial round trip (written by the GEMM, read by the fixed-order reduction: ~0.3 (S + 2) k-tile
   // waves of the tiles' share of the device)
-  const int64_t slots = gemm_slots<M, V, TA, TB>();
+  const int64_t slots = g_gemm_cta_cap > 0 ? std::min<int64_t>(g_gemm_cta_cap, gemm_slots<M, V, TA, TB>())
+                                           : gemm_slots<M, V, TA, TB>();
   const int64_t kt = cdiv(k, Tl::BK);
   int64_t S = 1;
   if (part && kt >= 4) {
@@ -252,8 +265,7 @@ void gemm_launch(cudaStream_t st, int64_t m, int64_t n, int64_t k, CMat A, CMat 
   int64_t kc = cdiv(cdiv(k, S), Tl::BK) * Tl::BK;
   S = std::max<int64_t>(1, cdiv(k, kc));
   GemmArgs g{m, n, k, A.p, A.ld, A.ps, B.p, B.ld, B.ps, C.p, C.ld, C.ps, mode, kc, S > 1 ? part : nullptr, S};
-  dim3 grid((unsigned)cdiv(n, Tl::BN), (unsigned)cdiv(m, Tl::BM), (unsigned)S);
-  gemm_kernel_launch<M, V, TA, TB>(st, grid, g);
+  gemm_kernel_launch<M, V, TA, TB>(st, g);
   if (S > 1)
     MDLS_LAUNCH(F_GEMM, st, splitk_reduce_kernel<M><<<grid_for(m * n, 256), 256, 0, st>>>(m, n, S, part, C.p, C.ld, C.ps, mode));
 }
@@ -326,8 +338,7 @@ void leaf_t_product(cudaStream_t st, int B, int64_t n, int64_t r, CMat Y, CMat T
   const int64_t kc = cdiv(cdiv(r, S), Tl::BK) * Tl::BK;
   S = std::max<int64_t>(1, cdiv(r, kc));
   GemmArgs g{B, n, r, Y.p, Y.ld, Y.ps, C.p, C.ld, C.ps, nullptr, B, 0, 0, kc, part, S};
-  dim3 grid((unsigned)cdiv(n, Tl::BN), (unsigned)cdiv(B, Tl::BM), (unsigned)S);
-  gemm_kernel_launch<M, 2, true, false>(st, grid, g);
+  gemm_kernel_launch<M, 2, true, false>(st, g);
   if (B == 16)
     MDLS_LAUNCH(F_GEMM, st, splitk_reduce_t_kernel<M, 16><<<(unsigned)cdiv(n, 16), 256, 0, st>>>(n, S, part, T, X.p, X.ld, X.ps));
   else

@@ -11,6 +11,7 @@
 // products over structural zeros) is NOT counted.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdint>
 #include <cstring>
@@ -52,22 +53,28 @@ cudaEvent_t get_event() {
 
 void set_stage(int stage) { t_stage = stage; }
 
-// two library-owned non-blocking side streams per device (joined into the
-// caller's stream by events in every call, so graph capture and ordering hold)
+// library-owned non-blocking side streams, kGroupStreams per group and kMaxGroups
+// groups per device (joined into the caller's stream by events in every call,
+// so graph capture and ordering hold)
 cudaStream_t side_stream(int which) {
-  // 0, 1, 4: high priority (QR critical chain, trailing applies it waits on); 2, 3, 5: low (W build, Q, inversion)
   static std::mutex mu;
-  static std::vector<cudaStream_t> streams;  // [device * 6 + which]
+  static std::vector<cudaStream_t> streams;  // [(device * kMaxGroups + group) * kGroupStreams + which]
   int dev = 0;
   cudaGetDevice(&dev);
+  const int w = which % kGroupStreams;
+  const int grp = g_stream_group % kMaxGroups;
   std::lock_guard<std::mutex> lk(mu);
-  const size_t idx = (size_t)dev * 6 + (size_t)(which % 6);
+  const size_t idx = ((size_t)dev * kMaxGroups + (size_t)grp) * kGroupStreams + (size_t)w;
   if (streams.size() <= idx) streams.resize(idx + 1, nullptr);
   if (!streams[idx]) {
     int least = 0, greatest = 0;
     cudaDeviceGetStreamPriorityRange(&least, &greatest);
-    const int w = which % 6;
-    cudaStreamCreateWithPriority(&streams[idx], cudaStreamNonBlocking, (w < 2 || w == 4) ? greatest : least);
+    // priority levels (greatest is numerically smallest): the leaf chain (0) above the near-window and
+    // far-window leaf updates (1, 5), inversion and the group main stream (6), above the W build and panel
+    // products (2, 4), above Q (3)
+    const int rank = (w == 0) ? 0 : (w == 1 || w == 5 || w == 6) ? 1 : (w == 3) ? 3 : 2;
+    const int prio = (rank == 3) ? least : std::min(least, greatest + rank);
+    cudaStreamCreateWithPriority(&streams[idx], cudaStreamNonBlocking, prio);
   }
   return streams[idx];
 }

@@ -51,8 +51,8 @@ Plan make_plan(int op, int64_t Mr, int64_t K, int64_t nb) {
   }
   if (op == MDLS_OP_APPLY_QT) p.y = take(md * Mr * K);
   if (qr_like || op == MDLS_OP_APPLY_QT) {
-    p.x = take(4 * md * nb * mx);  // one GEMM-intermediate buffer per stream lane
-    p.part = take(4 * md * kMaxSplit * nb * mx);
+    p.x = take(5 * md * nb * mx);  // one GEMM-intermediate buffer per stream lane
+    p.part = take(5 * md * kMaxSplit * nb * mx);
   }
   p.v0 = take(md * mx);
   p.v1 = take(md * mx);
@@ -83,7 +83,7 @@ struct QrBufs {
   double* part;
   int64_t part_cap;
   int* info_slot;
-  double* xbase;  // 3 lanes of X / part
+  double* xbase;  // 5 lanes of X / part
   double* pbase;
   int64_t xcap;
   Lane lane(int i, cudaStream_t st) const {
@@ -214,16 +214,24 @@ cudaError_t qr_factor_overlap(const Lane& L0, const Lane& L1, const Lane& L2, in
 
 // ---------------------------------------------------------------------------
 // Algorithm 2 as a chain of leaves (every leaf a register-leaf cluster kernel
-// that first applies the previous leaf to its own columns).  Streams (all
-// forked from and joined into `st`):
+// that first applies the previous leaf to its own columns), with the trailing
+// update split by distance.  Streams (all forked from and joined into `st`):
 //   Lc (high priority): the leaves -- the only serial path of the factorisation;
-//   La (high priority): per leaf s, W_s = -Y_s T_s and the trailing update
-//       C += Y_s (W_s^T C) of every column beyond leaf s+1 (leaf s+2 waits on it);
-//   Lw (low): the panel's W (the block recurrence W_s += W_<s (Y_<s^T W_s));
+//   La (high): per leaf s of panel k, C += Y_s X, X = -T_s^T (Y_s^T C), on the
+//       columns beyond leaf s+1 up to the end of panel k+1 (leaf s+2 waits on it);
+//   Lf (high): the same leaf update on the columns of panel k+2, one panel behind
+//       in its dependencies (it waits for panel k-1's product below);
+//   Lw (high): the panel's W (the block recurrence W_s += W_<s (Y_<s^T W_s));
+//   Lb (high): once W_k is complete, panel k's update of every column beyond
+//       panel k+2 as one k = nb product C += Y_k (W_k^T C) ("YWT * C",
+//       "R + YWTC"), the columns of panel k+3 first;
 //   Lq (low): the forward Q accumulation Q(:, j0:) += (Q(:, j0:) W_k) Y_k^T per
-//       completed panel when Qf is given.
-// Every (reflector, column) pair is applied exactly once, as in Algorithm 2;
-// only the grouping of the trailing update is per leaf instead of per panel.
+//       completed panel when Qf is given, on a capped number of CTAs
+//       (GemmCap) so that the chain's updates always find free CTA slots.
+// Every (reflector, column) pair is applied exactly once and every column sees
+// the reflectors in Algorithm 2's order: a column of panel k+3 gets panels <= k
+// through Lb, then panel k+1's leaves through Lf, panel k+2's through La, then
+// its own panel's leaves (in-leaf and the next leaf's prologue).
 // ---------------------------------------------------------------------------
 template <int M>
 bool chain_supported(int64_t Mr, int64_t K, int64_t nb) {
@@ -246,12 +254,10 @@ cudaError_t qr_factor_chain(cudaStream_t st, int64_t Mr, int64_t K, int64_t nb, 
     cudaEventRecord(ev, from);
     cudaStreamWaitEvent(to, ev, 0);
   };
-  cudaStream_t Lc = side_stream(0), Las = side_stream(1), Lws = side_stream(2), Lqs = side_stream(3);
-  const Lane La = b.lane(0, Las), Lw = b.lane(1, Lws), Lq = b.lane(2, Lqs);
-  fork(st, Lc);
-  fork(st, Las);
-  fork(st, Lws);
-  fork(st, Lqs);
+  cudaStream_t Lc = side_stream(0), Las = side_stream(1), Lws = side_stream(2), Lqs = side_stream(3),
+               Lbs = side_stream(4), Lfs = side_stream(5);
+  const Lane La = b.lane(0, Las), Lw = b.lane(1, Lws), Lq = b.lane(2, Lqs), Lb = b.lane(3, Lbs), Lf = b.lane(4, Lfs);
+  for (cudaStream_t q : {Lc, Las, Lws, Lqs, Lbs, Lfs}) fork(st, q);
   if (Qf) {
     set_stage(MDLS_ST_FORM_Q);
     MDLS_LAUNCH(F_MISC, Lqs, set_identity_kernel<M><<<grid_for(Mr * Mr, 256), 256, 0, Lqs>>>(Mr, Mr, *Qf));
@@ -266,7 +272,27 @@ cudaError_t qr_factor_chain(cudaStream_t st, int64_t Mr, int64_t K, int64_t nb, 
     js += B;
   }
   const int ns = (int)jss.size();
+  const int64_t N = K / nb;
+  // MDLS_DEFER=0: every leaf updates all trailing columns itself (no panel-level product)
+  static const bool defer = [] {
+    const char* v = getenv("MDLS_DEFER");
+    return !(v && v[0] == '0');
+  }();
+  // CTAs of the forward-Q products: by default one per SM outside the leaf's cluster (MDLS_QCAP)
+  static const int64_t qcap_env = [] {
+    const char* v = getenv("MDLS_QCAP");
+    return (int64_t)(v ? atoll(v) : -1);
+  }();
+  const int64_t qcap = qcap_env >= 0 ? qcap_env : std::max<int64_t>(1, num_sms() - leaf_cluster_size());
+  // CTAs of the panel products (Lb): MDLS_BCAP
+  static const int64_t bcap_env = [] {
+    const char* v = getenv("MDLS_BCAP");
+    return (int64_t)(v ? atoll(v) : -1);
+  }();
+  const int64_t bcap = bcap_env >= 0 ? bcap_env : 0;
   std::vector<cudaEvent_t> ev_apply((size_t)ns, nullptr);
+  std::vector<cudaEvent_t> ev_bulk_a((size_t)N, nullptr);  // Lb: panel k applied to the columns of panel k+3
+  std::vector<cudaEvent_t> ev_far((size_t)N, nullptr);     // Lf: panel k applied to the columns of panel k+2
   // MDLS_TIMELINE=1 (debug, not graph-capturable): per-leaf start/end and apply-end times, printed
   static const bool timeline = getenv("MDLS_TIMELINE") != nullptr;
   std::vector<cudaEvent_t> tl_ls, tl_le, tl_ae;
@@ -278,16 +304,30 @@ cudaError_t qr_factor_chain(cudaStream_t st, int64_t Mr, int64_t K, int64_t nb, 
     return e;
   };
   if (timeline) tl0 = tl_ev(Lc);
+  // leaf s's update C += Y_s X, X = -T_s^T (Y_s^T C), of the columns [c0, c1)
+  auto leaf_update = [&](const Lane& L, int s, int64_t c0, int64_t c1) {
+    if (c0 >= c1) return;
+    const int64_t js = jss[(size_t)s];
+    const int B = Bs[(size_t)s];
+    set_stage(MDLS_ST_TRAILING);
+    const Mat Cm = sub(A, js, c0);
+    const Mat Xb{L.X.p, B, L.X.ps};
+    const Mat Ts{Tall.p + js * 32, 32, Tall.ps};
+    leaf_t_product<M>(L.st, B, c1 - c0, Mr - js, sub(cm(b.Y), js, js), cm(Ts), cm(Cm), Xb, L.part, L.cap);
+    gemm<M, false, false>(L.st, Mr - js, c1 - c0, B, sub(cm(b.Y), js, js), cm(Xb), Cm, 1, nullptr, 0);
+  };
   cudaError_t err = cudaSuccess;
   for (int s = 0; s < ns && err == cudaSuccess; ++s) {
     const int64_t js = jss[(size_t)s];
     const int B = Bs[(size_t)s];
-    const int64_t j0 = (js / nb) * nb, r = Mr - js;
+    const int64_t k = js / nb, j0 = k * nb, r = Mr - js;
+    const bool first_in_panel = js == j0, last_in_panel = js + B == j0 + nb;
     const Mat Ts{Tall.p + js * 32, 32, Tall.ps};
     cudaEvent_t ev_leaf = pool_event();
     // Lc: leaf s (its prologue applies leaf s-1 to its own columns); leaf s-2 must have been applied to
-    // every column beyond leaf s-1 (La) first
+    // every column beyond leaf s-1 (La) first, and panel k-2 to this panel (Lf)
     if (s >= 2) cudaStreamWaitEvent(Lc, ev_apply[(size_t)s - 2], 0);
+    if (defer && first_in_panel && k >= 2 && ev_far[(size_t)k - 2]) cudaStreamWaitEvent(Lc, ev_far[(size_t)k - 2], 0);
     if (timeline) tl_ls.push_back(tl_ev(Lc));
     set_stage(MDLS_ST_PANEL);
     const Mat Tp = s > 0 ? Mat{Tall.p + jss[(size_t)s - 1] * 32, 32, Tall.ps} : Mat{nullptr, 0, 0};
@@ -295,44 +335,60 @@ cudaError_t qr_factor_chain(cudaStream_t st, int64_t Mr, int64_t K, int64_t nb, 
     if (err != cudaSuccess) break;
     cudaEventRecord(ev_leaf, Lc);
     if (timeline) tl_le.push_back(tl_ev(Lc));
-    // La: the trailing update of leaf s beyond leaf s+1, C += Y_s X with X = -T_s^T (Y_s^T C) (the T
-    // product folded into the split-K reduction, so W_s is not needed on this stream)
-    cudaStreamWaitEvent(Las, ev_leaf, 0);
-    const CMat Ys = sub(cm(b.Y), js, js);
     const int64_t c0 = (s + 1 < ns) ? jss[(size_t)s + 1] + Bs[(size_t)s + 1] : K;
-    if (c0 < K) {
-      set_stage(MDLS_ST_TRAILING);
-      const Mat Cm = sub(A, js, c0);
-      const Mat Xb{La.X.p, B, La.X.ps};
-      leaf_t_product<M>(Las, B, K - c0, r, Ys, cm(Ts), cm(Cm), Xb, La.part, La.cap);
-      gemm<M, false, false>(Las, r, K - c0, B, Ys, cm(Xb), Cm, 1, nullptr, 0);
-    }
+    // La: the near window, up to the end of panel k+1 (everything without deferral).  Panel k+1 has had
+    // panel k-1 applied by Lf (the first leaf of the panel waits for it; La is in order after that)
+    cudaStreamWaitEvent(Las, ev_leaf, 0);
+    if (defer && first_in_panel && k >= 1 && ev_far[(size_t)k - 1]) cudaStreamWaitEvent(Las, ev_far[(size_t)k - 1], 0);
+    const int64_t c1 = defer ? std::min<int64_t>(K, (k + 2) * nb) : K;
+    leaf_update(La, s, c0, c1);
     ev_apply[(size_t)s] = pool_event();
     cudaEventRecord(ev_apply[(size_t)s], Las);
     if (timeline) tl_ae.push_back(tl_ev(Las));
+    // Lf: panel k+2's columns, after panel k-1's product reached them (Lb)
+    if (defer && (k + 2) * nb < K) {
+      cudaStreamWaitEvent(Lfs, ev_leaf, 0);
+      if (first_in_panel && k >= 1 && ev_bulk_a[(size_t)k - 1]) cudaStreamWaitEvent(Lfs, ev_bulk_a[(size_t)k - 1], 0);
+      leaf_update(Lf, s, std::max<int64_t>(c0, (k + 2) * nb), std::min<int64_t>(K, (k + 3) * nb));
+    }
+    if (defer && last_in_panel) {
+      ev_far[(size_t)k] = pool_event();
+      cudaEventRecord(ev_far[(size_t)k], Lfs);
+    }
     // Lw: the panel's W, column block js..js+B-1
     cudaStreamWaitEvent(Lws, ev_leaf, 0);
     set_stage(MDLS_ST_WY);
-    gemm<M, false, false>(Lws, r, B, B, Ys, cm(Ts), sub(b.W, js, js), 3, nullptr, 0);
+    gemm<M, false, false>(Lws, r, B, B, sub(cm(b.Y), js, js), cm(Ts), sub(b.W, js, js), 3, nullptr, 0);
     if (js > j0) {
       const int64_t np = js - j0;
       gemm<M, true, false>(Lws, np, B, r, sub(cm(b.Y), js, j0), sub(cm(b.W), js, js), Lw.X, 0, Lw.part, Lw.cap);
       gemm<M, false, false>(Lws, Mr - j0, B, np, sub(cm(b.W), j0, j0), cm(Lw.X), sub(b.W, j0, js), 1, nullptr, 0);
     }
-    if (Qf && (js + B == j0 + nb || s == ns - 1)) {
-      fork(Lws, Lqs);
-      const int64_t k = js / nb;
-      form_q_forward_step<M>(Lq, Mr, nb, k, *Qf, sub(cm(b.Y), j0, j0), sub(cm(b.W), j0, j0));
+    if (last_in_panel || s == ns - 1) {
+      const CMat Yk = sub(cm(b.Y), j0, j0), Wk = sub(cm(b.W), j0, j0);
+      // Lb: panel k applied to the columns beyond panel k+2 (W_k complete on Lw)
+      const int64_t cb = (k + 3) * nb;
+      if (defer && cb < K) {
+        fork(Lws, Lbs);
+        GemmCap cap(bcap);
+        const int64_t cm1 = std::min<int64_t>(K, cb + nb);
+        qr_apply_panel<M>(Lb, Mr, nb, k, Yk, Wk, A, cb, cm1);
+        ev_bulk_a[(size_t)k] = pool_event();
+        cudaEventRecord(ev_bulk_a[(size_t)k], Lbs);
+        qr_apply_panel<M>(Lb, Mr, nb, k, Yk, Wk, A, cm1, K);
+      }
+      if (Qf) {
+        fork(Lws, Lqs);
+        GemmCap cap(qcap);
+        form_q_forward_step<M>(Lq, Mr, nb, k, *Qf, Yk, Wk);
+      }
     }
   }
   // join every side stream even on an error, so a caller's graph capture is never left forked
-  fork(Lc, st);
-  fork(Las, st);
-  fork(Lws, st);
-  fork(Lqs, st);
+  for (cudaStream_t q : {Lc, Las, Lws, Lqs, Lbs, Lfs}) fork(q, st);
   if (err != cudaSuccess) return err;
   if (timeline) {
-    cudaEvent_t tw = tl_ev(Lws), tq = tl_ev(Lqs);
+    cudaEvent_t tw = tl_ev(Lws), tq = tl_ev(Lqs), tb = tl_ev(Lbs), tf = tl_ev(Lfs);
     cudaDeviceSynchronize();
     float t;
     for (size_t s = 0; s < tl_ae.size(); ++s) {
@@ -343,10 +399,12 @@ cudaError_t qr_factor_chain(cudaStream_t st, int64_t Mr, int64_t K, int64_t nb, 
       printf("leaf %3zu start %8.1f end %8.1f (%6.1f us)  apply end %8.1f us\n", s, a0 * 1e3, a1 * 1e3,
              (a1 - a0) * 1e3, a2 * 1e3);
     }
-    cudaEventElapsedTime(&t, tl0, tw);
-    printf("W stream end %8.1f us\n", t * 1e3);
-    cudaEventElapsedTime(&t, tl0, tq);
-    printf("Q stream end %8.1f us\n", t * 1e3);
+    const char* names[4] = {"W", "Q", "panel-update", "far-window"};
+    cudaEvent_t evs[4] = {tw, tq, tb, tf};
+    for (int i = 0; i < 4; ++i) {
+      cudaEventElapsedTime(&t, tl0, evs[i]);
+      printf("%s stream end %8.1f us\n", names[i], t * 1e3);
+    }
   }
   return cudaGetLastError();
 }

@@ -30,7 +30,18 @@ enum Family { F_GEMM = 0, F_PANEL = 1, F_INVERT = 2, F_BS = 3, F_MISC = 4, F_NFA
 void trace_begin(cudaStream_t st, int family);
 void trace_end(cudaStream_t st, int family);
 void set_stage(int stage);
-// side streams / event pool for the look-ahead QR (ledger.cu)
+// side streams / event pool for the look-ahead QR (ledger.cu).  Streams come in
+// groups of kGroupStreams per device; side_stream(which) returns stream `which`
+// of the calling thread's current group (StreamGroup), so independent problems of
+// a batch run on disjoint stream sets and overlap on the device.
+constexpr int kGroupStreams = 8;  // 0..5: the QR lanes (solver.cuh), 6: the group's main stream
+constexpr int kMaxGroups = 16;
+inline thread_local int g_stream_group = 0;
+struct StreamGroup {
+  int prev;
+  explicit StreamGroup(int g) : prev(g_stream_group) { g_stream_group = g; }
+  ~StreamGroup() { g_stream_group = prev; }
+};
 cudaStream_t side_stream(int which);
 cudaEvent_t pool_event();
 #define MDLS_LAUNCH(FAM, ST, ...)          \
@@ -109,6 +120,17 @@ template <> struct GemmTile<8, 1> : Tile<16, 16, 16, 1, 1> {};
 template <> struct GemmTile<8, 2> : Tile<8, 32, 16, 1, 1> {};
 template <> struct GemmTile<8, 3> : Tile<32, 8, 16, 1, 1> {};
 constexpr int64_t kMaxSplitK = 64;
+
+// CTA cap of the md GEMMs issued by this host thread (0: none).  A capped product runs its
+// tiles in a grid-stride loop on at most that many CTAs, so a long low-priority product (the
+// forward Q accumulation) leaves CTA slots free for the latency-critical updates of the
+// factorisation chain.  Set with the RAII GemmCap.
+inline thread_local int64_t g_gemm_cta_cap = 0;
+struct GemmCap {
+  int64_t prev;
+  explicit GemmCap(int64_t cap) : prev(g_gemm_cta_cap) { g_gemm_cta_cap = cap; }
+  ~GemmCap() { g_gemm_cta_cap = prev; }
+};
 
 struct GemmArgs {
   int64_t m, n, k;
