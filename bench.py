@@ -36,7 +36,10 @@ WORKLOADS = {
     "cfg2": ("dd", 1024, 1024, 128),
     "cfg3qd": ("qd", 1024, 1024, 128),
     "cfg3od": ("od", 1024, 1024, 128),
+    "cfg5b": ("dd", 1024, 1024, 128),  # + BATCH_5B independent problems sharded over the ranks
 }
+BATCH_5B = 256
+BATCH_CHUNK = 32  # problems per captured CUDA graph (one mdls_lstsq_batched call each)
 METRIC = "md QR+backsub double-flops/s & % FP64 peak at n=1024 dd/qd/od, 1/2/4/8 B200"
 FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12      # 37.2 (FMA = 2 flops)
 FP64_PIPE_TOPS = 148 * 64 * 1.965e9 / 1e12            # 18.6 FP64-pipe lane ops/s (DADD/DMUL/DFMA each 1)
@@ -62,6 +65,8 @@ def parse():
     ap.add_argument("--no-extra", action="store_true", help="skip the qd/od side measurements")
     ap.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--groups", type=int, default=8, help="stream groups of the batched solves (cfg5b)")
+    ap.add_argument("--batch", type=int, default=BATCH_5B, help="problems of the cfg5b batch (all ranks)")
     return ap.parse_args()
 
 
@@ -209,36 +214,40 @@ def run_ours(args, ws, rank, local):
         return float(t.item())
 
     prec, M, K, nb = WORKLOADS[args.workload]
+    if args.workload == "cfg5b":
+        return run_batch_workload(args, ws, rank, dev, barrier, max_over_ranks)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
 
     def measure(prec, M, K, nb, steps, warmup, seed, with_e2e, with_trace, sampler=None):
         A_h, b_h = make_problem(prec, M, K, seed)
         A = torch.from_numpy(A_h).to(dev)
         b = torch.from_numpy(b_h).to(dev)
-        work = torch.empty(mdls.workspace_bytes(prec, 2, M, K, nb), dtype=torch.uint8, device=dev)
         stream = torch.cuda.current_stream()
+        # the solve as a library plan (mdls_lstsq_plan: the whole launch sequence captured once into a
+        # library-owned CUDA graph, replayed by one mdls_plan_launch per step); --no-graph: direct calls
+        plan = None
+        if not args.no_graph:
+            plan = mdls.LstsqPlan(prec, M, K, nb, form_q=True, device=dev)
+            plan.A.copy_(A)
+            plan.b.copy_(b)
+            work = plan.work
+        else:
+            work = torch.empty(mdls.workspace_bytes(prec, 2, M, K, nb), dtype=torch.uint8, device=dev)
 
         def step():
-            return mdls.lstsq(prec, A, b, nb, form_q=True, work=work)
+            if plan is not None:
+                plan.run()
+                return plan.info
+            return mdls.lstsq(prec, A, b, nb, form_q=True, work=work).info
 
         for _ in range(warmup):
-            r = step()
+            info = step()
         torch.cuda.synchronize()
-        assert int(r.info.item()) == 0, f"dev_info={int(r.info.item())}"
-        # capture one solve in a CUDA graph (launch-bound inner loops, no host work per step)
-        graph = None
+        assert int(info.item()) == 0, f"dev_info={int(info.item())}"
         n0 = mdls.launch_count()
-        if not args.no_graph:
-            graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph):
-                gr = step()
-            per_step_launches = mdls.launch_count() - n0
-            graph.replay()
-            torch.cuda.synchronize()
-        else:
-            step()
-            torch.cuda.synchronize()
-            per_step_launches = mdls.launch_count() - n0
+        step()
+        torch.cuda.synchronize()
+        per_step_launches = mdls.launch_count() - n0
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
         barrier()
         torch.cuda.synchronize()
@@ -247,10 +256,7 @@ def run_ours(args, ws, rank, local):
             for i in range(steps):
                 flush.fill_(float(i))  # L2 flush between timed steps (untimed)
                 ev[i][0].record(stream)
-                if graph is not None:
-                    graph.replay()
-                else:
-                    step()
+                step()
                 ev[i][1].record(stream)
             torch.cuda.synchronize()
         barrier()
@@ -261,7 +267,7 @@ def run_ours(args, ws, rank, local):
             mdls.trace_enable(True)
             for i in range(steps):
                 flush.fill_(float(i))
-                step()
+                mdls.lstsq(prec, A, b, nb, form_q=True, work=work)
             torch.cuda.synchronize()
             mdls.trace_enable(False)
             tr = mdls.trace_collect()
@@ -271,23 +277,28 @@ def run_ours(args, ws, rank, local):
             A_p = torch.from_numpy(A_h).pin_memory()
             b_p = torch.from_numpy(b_h).pin_memory()
             x_p = torch.empty((A_h.shape[0], K), dtype=torch.float64).pin_memory()
-            A_d = torch.empty_like(A)
-            b_d = torch.empty_like(b)
-            for _ in range(2):
+            if plan is None:
+                A_d, b_d = torch.empty_like(A), torch.empty_like(b)
+
+            def e2e_step():
+                if plan is not None:
+                    x_p.copy_(plan.solve(A_p, b_p), non_blocking=True)
+                    return plan.info
                 A_d.copy_(A_p, non_blocking=True)
                 b_d.copy_(b_p, non_blocking=True)
                 rr = mdls.lstsq(prec, A_d, b_d, nb, form_q=True, work=work)
                 x_p.copy_(rr.x, non_blocking=True)
+                return rr.info
+
+            for _ in range(2):
+                e2e_step()
             torch.cuda.synchronize()
             barrier()
             t0 = torch.cuda.Event(enable_timing=True)
             t1 = torch.cuda.Event(enable_timing=True)
             t0.record(stream)
             for _ in range(steps):
-                A_d.copy_(A_p, non_blocking=True)
-                b_d.copy_(b_p, non_blocking=True)
-                rr = mdls.lstsq(prec, A_d, b_d, nb, form_q=True, work=work)
-                x_p.copy_(rr.x, non_blocking=True)
+                info = e2e_step()
             t1.record(stream)
             torch.cuda.synchronize()
             barrier()
@@ -295,7 +306,8 @@ def run_ours(args, ws, rank, local):
             out["h2d"] = A_h.nbytes + b_h.nbytes
             out["d2h"] = x_p.numel() * 8
             # parity guard on the e2e result (cheap invariant: finite, dev_info 0)
-            assert int(rr.info.item()) == 0 and bool(np.isfinite(x_p.numpy()).all())
+            assert int(info.item()) == 0 and bool(np.isfinite(x_p.numpy()).all())
+        del plan
         return out
 
     sampler = ClockSampler(local)
@@ -327,7 +339,7 @@ def run_ours(args, ws, rank, local):
             "precision": prec, "M": M, "K": K, "nb": nb,
             "parallelism": f"batch{ws}" if ws > 1 else "single",
             "l2": f"flushed between timed steps ({L2_FLUSH_BYTES >> 20} MiB write, untimed)",
-            "graph": not args.no_graph,
+            "graph": "library plan (mdls_lstsq_plan: one CUDA graph replay per step)" if not args.no_graph else False,
             "flops_per_solve": flops,
         },
         "fp64_peak_frac": round(value / ws / (FP64_PEAK_TFLOPS * 1e3), 4),
@@ -381,10 +393,54 @@ def run_ours(args, ws, rank, local):
             "qd_to_od": round(extra["od"]["ms_per_solve"] / extra["qd"]["ms_per_solve"], 2),
             "predicted_T1": {"dd_to_qd": 11.7, "qd_to_od": 5.4},
         }
+    if not args.no_extra and args.workload == "cfg2" and ws == 1:
+        rb = bench_batch(dev, prec, M, K, nb, BATCH_CHUNK, args.groups, max(2, min(args.steps, 5)), 1, 0, 1,
+                         lambda: None, lambda v: v, args.no_graph)
+        fb = ledger_flops(prec, M, K, nb)["total_flops"] * BATCH_CHUNK
+        vb = fb / (rb["ms_per_step"] * 1e-3) / 1e9
+        res["batch_cfg5b_1gpu"] = {
+            "workload": f"{BATCH_CHUNK} independent {prec} {M}x{K} solves, one mdls_lstsq_batched call, "
+                        f"{rb['groups']} stream groups (config 5b's per-GPU unit)",
+            "ms_per_batch": round(rb["ms_per_step"], 3), "ms_per_solve": round(rb["ms_per_solve_per_gpu"], 4),
+            "gflops": round(vb, 2), "fp64_peak_frac": round(vb / (FP64_PEAK_TFLOPS * 1e3), 4)}
     if not args.no_extra and args.workload == "cfg2":
         res["backsub_cfg4"] = bench_backsub(dev, "qd", 17920, 128, max(3, min(args.steps, 10)), 2, args.no_graph)
     if rank == 0 and ws == 1 and not args.no_cpu:
         res["cpu_baseline"] = cpu_baseline(prec, M, K, nb)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+
+
+def run_batch_workload(args, ws, rank, dev, barrier, max_over_ranks):
+    """--workload cfg5b: BASELINE config 5b, a batch of args.batch independent dd 1024 x 1024 solves sharded
+    over the ranks (fixed total: strong scaling), no data-path collective."""
+    prec, M, K, nb = WORKLOADS["cfg5b"]
+    sampler = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
+    r = bench_batch(dev, prec, M, K, nb, args.batch, args.groups, args.steps, args.warmup, rank, ws, barrier,
+                    max_over_ranks, args.no_graph, sampler=sampler, with_e2e=True)
+    flops = ledger_flops(prec, M, K, nb)["total_flops"] * args.batch
+    value = flops / (r["ms_per_step"] * 1e-3) / 1e9
+    res = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(r["ms_per_step"], 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"batch of {args.batch} independent {prec} least squares {M}x{K}, tile {nb}, "
+                               f"sharded over {ws} GPU(s) (mdls_lstsq_batched, {r['groups']} stream groups)",
+                   "precision": prec, "M": M, "K": K, "nb": nb, "batch": args.batch,
+                   "parallelism": f"batch-shard{ws}", "l2": "inputs exceed L2 (no flush)", "graph": not args.no_graph,
+                   "flops_per_solve": flops / args.batch},
+        "fp64_peak_frac": round(value / ws / (FP64_PEAK_TFLOPS * 1e3), 4),
+        "fp64_peak_tflops": round(FP64_PEAK_TFLOPS, 2),
+        "ms_per_solve_per_gpu": round(r["ms_per_solve_per_gpu"], 4),
+        "clocks": sampler.summary(),
+        "e2e": {"value": round(flops / (r["e2e_ms"] * 1e-3) / 1e9, 2), "unit": "GFLOP/s",
+                "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"], "ms_per_step": round(r["e2e_ms"], 3)},
+        "gpu_launches": int(r["launches_per_step"] * args.steps),
+    }
     if ws > 1:
         import torch.distributed as dist
 
@@ -457,6 +513,86 @@ def bench_backsub(dev, prec, n, nb, steps, warmup, no_graph):
         "paper_V100_tiling": "80 x 224",
         "speedup_vs_V100_kernel_time": round(237.1 / ms, 1),
     }
+
+
+def bench_batch(dev, prec, M, K, nb, total, groups, steps, warmup, rank, ws, barrier, max_over_ranks, no_graph,
+                sampler=None, with_e2e=False):
+    """Independent problems p = 0..total-1 (seed p), rank r solving its shard_range block with
+    mdls_lstsq_batched plans (chunks of BATCH_CHUNK problems, one plan each)."""
+    import numpy as np
+    import torch
+
+    import paper_2110_08375_b200 as mdls
+    from paper_2110_08375_b200 import batch
+
+    lo, hi = batch.shard_range(total, rank, ws)
+    nloc = hi - lo
+    G = max(1, min(groups, 16))
+    chunks = [(c, min(nloc, c + BATCH_CHUNK)) for c in range(0, nloc, BATCH_CHUNK)]
+    # one plan per chunk (mdls_lstsq_batched_plan: the chunk's solves captured into a library-owned CUDA graph);
+    # each plan owns its chunk's A, b, x; problem p generated from seed p
+    plans, A_h, b_h = [], [], []
+    for c0, c1 in chunks:
+        probs = [make_problem(prec, M, K, lo + p) for p in range(c0, c1)]
+        ah = np.stack([a for a, _ in probs])
+        bh = np.stack([bb for _, bb in probs])
+        del probs
+        pl = mdls.BatchedLstsqPlan(prec, c1 - c0, M, K, nb, form_q=True, groups=G, device=dev)
+        pl.A.copy_(torch.from_numpy(ah))
+        pl.b.copy_(torch.from_numpy(bh))
+        plans.append(pl)
+        if with_e2e:
+            A_h.append(torch.from_numpy(ah).pin_memory())
+            b_h.append(torch.from_numpy(bh).pin_memory())
+    launches = sum(pl.launches for pl in plans)
+
+    def step():
+        for pl in plans:
+            pl.run()
+
+    for _ in range(max(1, warmup)):
+        step()
+    torch.cuda.synchronize()
+    for pl in plans:
+        assert int(pl.info.abs().sum()) == 0
+    stream = torch.cuda.current_stream()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    barrier()
+    torch.cuda.synchronize()
+    with (sampler if sampler is not None else _Null()):
+        for i in range(steps):
+            ev[i][0].record(stream)
+            step()  # inputs (16.8 MB per problem x problems per rank) exceed L2: no flush needed
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = max_over_ranks(sum(a.elapsed_time(bb) for a, bb in ev) / steps)
+    out = {"ms_per_step": ms, "problems_total": total, "problems_per_rank_max": -(-total // ws), "groups": G,
+           "launches_per_step": launches, "ms_per_solve_per_gpu": ms / max(1, -(-total // ws))}
+    if with_e2e:  # public API from pinned host buffers: inputs copied in, plan replayed, solutions copied out
+        x_p = [torch.empty(tuple(pl.x.shape), dtype=torch.float64).pin_memory() for pl in plans]
+
+        def e2e_step():
+            for pl, ah, bh, xp in zip(plans, A_h, b_h, x_p):
+                xp.copy_(pl.solve(ah, bh), non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(steps):
+            e2e_step()
+        t1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        out["e2e_ms"] = max_over_ranks(t0.elapsed_time(t1) / steps)
+        out["h2d"] = sum(t.numel() * 8 for t in A_h + b_h)
+        out["d2h"] = sum(t.numel() * 8 for t in x_p)
+        assert all(bool(torch.isfinite(t).all()) for t in x_p)
+    del plans
+    torch.cuda.empty_cache()
+    return out
 
 
 class _Null:

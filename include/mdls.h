@@ -103,6 +103,17 @@ int mdls_limbs(int prec_index /* 0 dd, 1 qd, 2 od */);
  *   2 tile inversion, 3 back substitution, 4 other), release the events.
  *   Returns the number of launches collected or MDLS_ERR_CUDA. Arrays may be NULL. */
 int64_t mdls_launch_count(void);
+
+/* Plans (library-owned CUDA graphs).  mdls_lstsq_plan_<p> / mdls_lstsq_batched_plan_<p> take the arguments of
+ * the direct call (minus the stream) and capture its whole launch sequence once, on a library stream of the
+ * current device, into an instantiated CUDA graph returned in *plan; the buffers (A, b, x, work, dev_info) are
+ * fixed at capture and must stay allocated while the plan lives.  Nothing runs at creation.
+ * mdls_plan_launch enqueues one replay on `stream` (one host call for the hundreds of kernels of a solve;
+ * stream-ordered like the direct call).  Returns 0 or MDLS_ERR_CUDA; -1 for a NULL plan.
+ * mdls_plan_launches: library kernels per replay.  mdls_plan_destroy releases the graph (NULL is a no-op). */
+int mdls_plan_launch(void *plan, void *stream);
+int64_t mdls_plan_launches(void *plan);
+void mdls_plan_destroy(void *plan);
 void mdls_trace_enable(int on);
 int mdls_trace_collect(double *stage_ms, double *family_ms, int64_t *family_launches);
 
@@ -114,7 +125,9 @@ int mdls_trace_collect(double *stage_ms, double *family_ms, int64_t *family_laun
   int mdls_count_##P(int op, int64_t M, int64_t K, int64_t nb, mdls_counts *out);                                  \
                                                                                                                    \
   /* A0: elementwise md arithmetic on device vectors (op: 0 add, 1 sub, 2 mul, 3 div, 4 sqrt, 5 latency-lean sqrt, \
-   * 6 latency-lean reciprocal 1/a -- the panel's Newton/Karp variants; b unused for ops >= 4).                      \
+   * 6 latency-lean reciprocal 1/a -- the panel's Newton/Karp variants; 7 mul, 8 latency-lean sqrt, 9 latency-lean  \
+   * reciprocal computed by one warp per entry (md_warp.cuh: the panel's warp-cooperative qd/od scalar chain; dd    \
+   * falls back to ops 2/5/6); b unused for ops 4-6, 8, 9).                                                          \
    * c = a op b, n entries, planes ps apart (same ps for a, b, c).  The operations are the readings of              \
    * DESIGN.md. */                                                                                       \
   int mdls_md_op_##P(int op, int64_t n, const double *a, const double *b, double *c, int64_t ps, void *stream);     \
@@ -184,6 +197,14 @@ int mdls_trace_collect(double *stage_ms, double *family_ms, int64_t *family_laun
                              int64_t psa, int64_t strideA, const double *b, int64_t psb, int64_t strideB,          \
                              double *x, int64_t psx, int64_t strideX, int form_q, int groups, void *work,          \
                              size_t work_bytes, int *dev_info, void *stream);                                      \
+  /* plan versions of mdls_lstsq_<p> and mdls_lstsq_batched_<p> (see "Plans" above); *plan = NULL on error. */  \
+  int mdls_lstsq_plan_##P(int64_t M, int64_t K, int64_t nb, const double *A, int64_t lda, int64_t psa,            \
+                          const double *b, int64_t psb, double *x, int64_t psx, int form_q, void *work,             \
+                          size_t work_bytes, int *dev_info, void **plan);                                          \
+  int mdls_lstsq_batched_plan_##P(int64_t batch, int64_t M, int64_t K, int64_t nb, const double *A, int64_t lda,  \
+                                  int64_t psa, int64_t strideA, const double *b, int64_t psb, int64_t strideB,     \
+                                  double *x, int64_t psx, int64_t strideX, int form_q, int groups, void *work,     \
+                                  size_t work_bytes, int *dev_info, void **plan);                                  \
   /* bytes of `work` for mdls_lstsq_batched_<p> (op MDLS_OP_LSTSQ or MDLS_OP_LSTSQ_NOQ); 0 for invalid sizes. */ \
   size_t mdls_workspace_batched_##P(int op, int64_t M, int64_t K, int64_t nb, int groups);                        \
                                                                                                                    \

@@ -16,7 +16,8 @@ import ctypes
 from . import _lib
 
 PRECISIONS = {"dd": 2, "qd": 4, "od": 8}
-OPS = {"add": 0, "sub": 1, "mul": 2, "div": 3, "sqrt": 4, "sqrt_fast": 5, "recip_fast": 6}
+OPS = {"add": 0, "sub": 1, "mul": 2, "div": 3, "sqrt": 4, "sqrt_fast": 5, "recip_fast": 6, "wmul": 7, "wsqrt_fast": 8,
+       "wrecip_fast": 9}
 T1_SUMS = {"dd": (20, 23, 70), "qd": (89, 336, 893), "od": (269, 1742, 5126)}  # P:102-136 (add, mul, div)
 
 __all__ = ["md_op", "qr", "apply_qt", "qt_b", "invert_tiles", "backsub", "lstsq", "norm2", "counts",
@@ -78,7 +79,7 @@ def md_op(op: str, prec: str, a, b=None):
     """Elementwise md arithmetic on (m, n) CUDA vectors (A0)."""
     torch = _torch()
     _check_md(a, prec, 2, "a")
-    unary = OPS[op] >= 4
+    unary = OPS[op] >= 4 and OPS[op] != 7
     if not unary:
         _check_md(b, prec, 2, "b")
     c = torch.empty_like(a)
@@ -261,6 +262,96 @@ def lstsq_batched(prec: str, A, b, nb: int, form_q: bool = True, groups: int = 4
                                               _ptr(info), _stream())
     _lib.check(rc, "lstsq_batched")
     return x, info[:Bn]
+
+
+class _Plan:
+    """Owner of a libmdls plan (a library-owned CUDA graph of one call) and of the device buffers it was
+    captured with.  run() replays it on the current stream."""
+
+    def _capture(self, fn, args):
+        h = ctypes.c_void_p(0)
+        rc = fn(*args, ctypes.byref(h))
+        _lib.check(rc, "plan")
+        self._h = h
+
+    def run(self):
+        rc = _lib.load().mdls_plan_launch(self._h, _stream())
+        _lib.check(rc, "plan_launch")
+
+    @property
+    def launches(self) -> int:
+        return int(_lib.load().mdls_plan_launches(self._h))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                _lib.load().mdls_plan_destroy(h)
+            except Exception:  # pragma: no cover (interpreter shutdown)
+                pass
+
+
+class LstsqPlan(_Plan):
+    """Least squares of one M x K shape as a replayable plan (mdls_lstsq_plan_<p>): the plan owns A (m, K, M),
+    b (m, M), x (m, K), info and the workspace.  solve(A, b) copies the inputs in (device tensors or pinned host
+    tensors, asynchronously), replays the captured solve and returns x (the plan's buffer; copy it before the
+    next solve)."""
+
+    def __init__(self, prec: str, M: int, K: int, nb: int, form_q: bool = True, device=None):
+        torch = _torch()
+        dev = torch.device("cuda") if device is None else torch.device(device)
+        m = PRECISIONS[prec]
+        self.prec, self.M, self.K, self.nb = prec, M, K, nb
+        self.A = torch.zeros((m, K, M), dtype=torch.float64, device=dev)
+        self.b = torch.zeros((m, M), dtype=torch.float64, device=dev)
+        self.x = torch.empty((m, K), dtype=torch.float64, device=dev)
+        self.info = torch.zeros(1, dtype=torch.int32, device=dev)
+        op = _lib.OP_LSTSQ if form_q else _lib.OP_LSTSQ_NOQ
+        self.work, nbytes = _work(prec, op, M, K, nb, dev)
+        self._capture(_lib.fn("mdls_lstsq_plan_", prec),
+                      (M, K, nb, *_mat(self.A), *_vec(self.b), *_vec(self.x), int(form_q), _ptr(self.work), nbytes,
+                       _ptr(self.info)))
+
+    def solve(self, A=None, b=None):
+        if A is not None:
+            self.A.copy_(A, non_blocking=True)
+        if b is not None:
+            self.b.copy_(b, non_blocking=True)
+        self.run()
+        return self.x
+
+
+class BatchedLstsqPlan(_Plan):
+    """mdls_lstsq_batched_plan_<p>: `batch` problems of one shape on `groups` stream groups, as one plan; owns
+    A (B, m, K, M), b (B, m, M), x (B, m, K), info (B,) and the workspace."""
+
+    def __init__(self, prec: str, batch: int, M: int, K: int, nb: int, form_q: bool = True, groups: int = 8,
+                 device=None):
+        torch = _torch()
+        dev = torch.device("cuda") if device is None else torch.device(device)
+        m = PRECISIONS[prec]
+        self.prec, self.batch, self.M, self.K, self.nb = prec, batch, M, K, nb
+        self.A = torch.zeros((batch, m, K, M), dtype=torch.float64, device=dev)
+        self.b = torch.zeros((batch, m, M), dtype=torch.float64, device=dev)
+        self.x = torch.empty((batch, m, K), dtype=torch.float64, device=dev)
+        self.info = torch.zeros(max(batch, 1), dtype=torch.int32, device=dev)
+        op = _lib.OP_LSTSQ if form_q else _lib.OP_LSTSQ_NOQ
+        groups = max(1, min(int(groups), 16))
+        nbytes = batch_workspace_bytes(prec, op, M, K, nb, groups)
+        if nbytes == 0:
+            raise ValueError("invalid batched least-squares shape")
+        self.work = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        self._capture(_lib.fn("mdls_lstsq_batched_plan_", prec),
+                      (batch, M, K, nb, _ptr(self.A), M, K * M, m * K * M, _ptr(self.b), M, m * M, _ptr(self.x), K,
+                       m * K, int(form_q), groups, _ptr(self.work), nbytes, _ptr(self.info)))
+
+    def solve(self, A=None, b=None):
+        if A is not None:
+            self.A.copy_(A, non_blocking=True)
+        if b is not None:
+            self.b.copy_(b, non_blocking=True)
+        self.run()
+        return self.x
 
 
 def launch_count() -> int:

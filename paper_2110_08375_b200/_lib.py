@@ -51,13 +51,16 @@ _SIGS = {
     "mdls_norm2_": (_I, [_L, _P, _L, _P, _L, _P]),
     "mdls_lstsq_batched_": (_I, [_L, _L, _L, _L, _P, _L, _L, _L, _P, _L, _L, _P, _L, _L, _I, _I, _P, _Z, _P, _P]),
     "mdls_workspace_batched_": (_Z, [_I, _L, _L, _L, _I]),
+    "mdls_lstsq_plan_": (_I, [_L, _L, _L, _P, _L, _L, _P, _L, _P, _L, _I, _P, _Z, _P, ctypes.POINTER(_P)]),
+    "mdls_lstsq_batched_plan_": (_I, [_L, _L, _L, _L, _P, _L, _L, _L, _P, _L, _L, _P, _L, _L, _I, _I, _P, _Z, _P,
+                                      ctypes.POINTER(_P)]),
     "mdls_qr_panel_": (_I, [_L, _L, _L, _P, _L, _L, _P, _L, _L, _P, _L, _L, _P, _Z, _P, _P]),
     "mdls_qr_update_": (_I, [_L, _L, _L, _P, _L, _L, _P, _L, _L, _P, _L, _L, _L, _L, _P, _Z, _P]),
 }
 
 # every symbol include/mdls.h declares
 EXPORTED = ["mdls_strerror", "mdls_version", "mdls_limbs", "mdls_launch_count", "mdls_trace_enable",
-            "mdls_trace_collect"] + [f"{n}{p}" for n in _SIGS for p in PRECS]
+            "mdls_trace_collect", "mdls_plan_launch", "mdls_plan_launches", "mdls_plan_destroy"] + [f"{n}{p}" for n in _SIGS for p in PRECS]
 
 _lib: ctypes.CDLL | None = None
 
@@ -81,6 +84,12 @@ def load() -> ctypes.CDLL:
     lib.mdls_trace_enable.restype = None
     lib.mdls_trace_collect.argtypes = [_P, _P, _P]
     lib.mdls_trace_collect.restype = _I
+    lib.mdls_plan_launch.argtypes = [_P, _P]
+    lib.mdls_plan_launch.restype = _I
+    lib.mdls_plan_launches.argtypes = [_P]
+    lib.mdls_plan_launches.restype = _L
+    lib.mdls_plan_destroy.argtypes = [_P]
+    lib.mdls_plan_destroy.restype = None
     for name, (res, args) in _SIGS.items():
         for p in PRECS:
             f = getattr(lib, f"{name}{p}")

@@ -16,7 +16,7 @@ CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libmdls.so")
 SOURCES = [f"{k}_{p}.cu" for p in ("od", "qd", "dd") for k in ("panel", "leafsm", "gemm", "bs", "api")] + ["ledger.cu"]
-HEADERS = ["md.cuh", "types.cuh", "launch.cuh", "kern_misc.cuh", "kern_gemm.cuh", "kern_leaf.cuh", "kern_bs.cuh",
+HEADERS = ["md.cuh", "md_warp.cuh", "types.cuh", "launch.cuh", "kern_misc.cuh", "kern_gemm.cuh", "kern_leaf.cuh", "kern_bs.cuh",
            "solver.cuh", "api.cuh"]
 
 NVCC_FLAGS = [

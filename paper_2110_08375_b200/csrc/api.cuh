@@ -81,14 +81,17 @@ size_t MDLS_FN(mdls_workspace_)(int op, int64_t Mr, int64_t K, int64_t nb) {
 }
 
 int MDLS_FN(mdls_md_op_)(int op, int64_t n, const double* a, const double* b, double* c, int64_t ps, void* stream) {
-  if (op < 0 || op > 6) return -1;
+  if (op < 0 || op > 9) return -1;
   if (n < 0) return -2;
   if (n == 0) return 0;
   if (!a) return -3;
-  if (!b && op < 4) return -4;
+  if (!b && (op < 4 || op == 7)) return -4;
   if (!c) return -5;
   if (ps < n) return -6;
-  MDLS_LAUNCH(F_MISC, S(stream), md_op_kernel<M><<<grid_for(n, 128), 128, 0, S(stream)>>>(op, n, a, b, c, ps));
+  if (op >= 7)
+    MDLS_LAUNCH(F_MISC, S(stream), md_op_warp_kernel<M><<<grid_for(32 * n, 128), 128, 0, S(stream)>>>(op, n, a, b, c, ps));
+  else
+    MDLS_LAUNCH(F_MISC, S(stream), md_op_kernel<M><<<grid_for(n, 128), 128, 0, S(stream)>>>(op, n, a, b, c, ps));
   return launched();
 }
 
@@ -335,12 +338,10 @@ int MDLS_FN(mdls_lstsq_)(int64_t Mr, int64_t K, int64_t nb, const double* A, int
                    psy, work, dev_info);
 }
 
-// independent least-squares problems p = 0..batch-1 (A_p = A + p*strideA, b_p, x_p likewise):
-// problem p runs on stream group p mod G with workspace slice p mod G, so G solves overlap on the device
-int MDLS_FN(mdls_lstsq_batched_)(int64_t batch, int64_t Mr, int64_t K, int64_t nb, const double* A, int64_t lda,
-                                 int64_t psa, int64_t strideA, const double* b, int64_t psb, int64_t strideB,
-                                 double* x, int64_t psx, int64_t strideX, int form_q, int groups, void* work,
-                                 size_t work_bytes, int* dev_info, void* stream) {
+// host argument checks of mdls_lstsq_batched_<p> (-i = argument i)
+static int batched_check(int64_t batch, int64_t Mr, int64_t K, int64_t nb, const double* A, int64_t lda, int64_t psa,
+                         int64_t strideA, const double* b, int64_t psb, int64_t strideB, const double* x, int64_t psx,
+                         int64_t strideX, int form_q, int groups, const void* work, size_t work_bytes) {
   if (batch < 0) return -1;
   if (int e = tile_ok(Mr, K, nb)) return e - 1;
   if (!mat_ok(A, Mr, K, lda, psa)) return -5;
@@ -351,8 +352,21 @@ int MDLS_FN(mdls_lstsq_batched_)(int64_t batch, int64_t Mr, int64_t K, int64_t n
   if (strideX < (M - 1) * psx + K) return -14;
   if (groups < 1 || groups > kMaxGroups) return -16;
   const int op = form_q ? MDLS_OP_LSTSQ : MDLS_OP_LSTSQ_NOQ;
+  if (!work || work_bytes < align256(make_plan<M>(op, Mr, K, nb).total) * (size_t)groups) return -18;
+  return 0;
+}
+
+// independent least-squares problems p = 0..batch-1 (A_p = A + p*strideA, b_p, x_p likewise):
+// problem p runs on stream group p mod G with workspace slice p mod G, so G solves overlap on the device
+int MDLS_FN(mdls_lstsq_batched_)(int64_t batch, int64_t Mr, int64_t K, int64_t nb, const double* A, int64_t lda,
+                                 int64_t psa, int64_t strideA, const double* b, int64_t psb, int64_t strideB,
+                                 double* x, int64_t psx, int64_t strideX, int form_q, int groups, void* work,
+                                 size_t work_bytes, int* dev_info, void* stream) {
+  if (int e = batched_check(batch, Mr, K, nb, A, lda, psa, strideA, b, psb, strideB, x, psx, strideX, form_q, groups,
+                            work, work_bytes))
+    return e;
+  const int op = form_q ? MDLS_OP_LSTSQ : MDLS_OP_LSTSQ_NOQ;
   const size_t slice = align256(make_plan<M>(op, Mr, K, nb).total);
-  if (!work || work_bytes < slice * (size_t)groups) return -18;
   if (batch == 0) return 0;
   cudaStream_t st = S(stream);
   const int G = (int)std::min<int64_t>(groups, batch);
@@ -378,6 +392,50 @@ int MDLS_FN(mdls_lstsq_batched_)(int64_t batch, int64_t Mr, int64_t K, int64_t n
     cudaStreamWaitEvent(st, ev, 0);
   }
   return rc;
+}
+
+// plans: the same calls captured once into a library-owned CUDA graph (buffers fixed at capture);
+// mdls_plan_launch replays them with one host call
+int MDLS_FN(mdls_lstsq_plan_)(int64_t Mr, int64_t K, int64_t nb, const double* A, int64_t lda, int64_t psa,
+                              const double* b, int64_t psb, double* x, int64_t psx, int form_q, void* work,
+                              size_t work_bytes, int* dev_info, void** plan) {
+  if (!plan) return -15;
+  *plan = nullptr;
+  if (int e = tile_ok(Mr, K, nb)) return e;
+  if (!mat_ok(A, Mr, K, lda, psa)) return -4;
+  if (!b || psb < Mr) return -7;
+  if (!x || psx < K) return -9;
+  const int op = form_q ? MDLS_OP_LSTSQ : MDLS_OP_LSTSQ_NOQ;
+  if (!work || work_bytes < make_plan<M>(op, Mr, K, nb).total) return -13;
+  cudaStream_t cs = capture_begin();
+  if (!cs) return MDLS_ERR_CUDA;
+  const int64_t n0 = mdls_launch_count();
+  const int rc = lstsq_run(cs, Mr, K, nb, A, lda, psa, b, psb, x, psx, form_q, nullptr, 0, 0, nullptr, 0, 0, nullptr,
+                           0, work, dev_info);
+  const int rc2 = capture_end(cs, mdls_launch_count() - n0, plan);
+  return rc ? rc : rc2;
+}
+
+int MDLS_FN(mdls_lstsq_batched_plan_)(int64_t batch, int64_t Mr, int64_t K, int64_t nb, const double* A,
+                                      int64_t lda, int64_t psa, int64_t strideA, const double* b, int64_t psb,
+                                      int64_t strideB, double* x, int64_t psx, int64_t strideX, int form_q,
+                                      int groups, void* work, size_t work_bytes, int* dev_info, void** plan) {
+  if (!plan) return -20;
+  *plan = nullptr;
+  if (int e = batched_check(batch, Mr, K, nb, A, lda, psa, strideA, b, psb, strideB, x, psx, strideX, form_q, groups,
+                            work, work_bytes))
+    return e;
+  cudaStream_t cs = capture_begin();
+  if (!cs) return MDLS_ERR_CUDA;
+  const int64_t n0 = mdls_launch_count();
+  const int rc = MDLS_FN(mdls_lstsq_batched_)(batch, Mr, K, nb, A, lda, psa, strideA, b, psb, strideB, x, psx,
+                                              strideX, form_q, groups, work, work_bytes, dev_info, cs);
+  const int rc2 = capture_end(cs, mdls_launch_count() - n0, plan);
+  if (rc && *plan) {
+    mdls_plan_destroy(*plan);
+    *plan = nullptr;
+  }
+  return rc ? rc : rc2;
 }
 
 size_t MDLS_FN(mdls_workspace_batched_)(int op, int64_t Mr, int64_t K, int64_t nb, int groups) {

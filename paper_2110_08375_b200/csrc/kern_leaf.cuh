@@ -20,6 +20,7 @@
 #include <cstdio>
 
 #include "launch.cuh"
+#include "md_warp.cuh"
 
 namespace mdls {
 
@@ -870,16 +871,24 @@ __device__ __forceinline__ void leaf_body(const LeafArgs<M>& a, bool init_bars, 
         }
       }
     } else {
-      // qd/od, phase A: mu and s = x1 +- mu (thread 0), 1/sigma (warp 1), 1/mu = rsqrt(x1^2 + sigma) (warp 2)
+      // qd/od, phase A: every md product of the scalar chain is taken by a whole warp (md_warp.cuh):
+      // warp 0: mu = sqrt(x1^2 + sigma), s = x1 +- mu; warp 1: 1/sigma (x1 > 0); warp 2: 1/mu = rsqrt(x1^2 + sigma)
       if (!deg) {
-        if (tid == 0) {
-          const md<M> mu = sqrt_fast<M>(add<M>(mul<M>(x1, x1), sigma));
-          sc_mu = mu;
-          sc_s = pos ? add<M>(x1, mu) : sub<M>(x1, mu);
-        } else if (tid == 32) {
-          if (pos) sc_rsig = recip_fast<M>(sigma);
-        } else if (tid == 64) {
-          sc_rmu = rsqrt_md<M>(add<M>(mul<M>(x1, x1), sigma));
+        if (warp == 0) {
+          const md<M> mu = w_sqrt_fast<M>(add<M>(wmul<M>(x1, x1), sigma));
+          const md<M> sv = pos ? add<M>(x1, mu) : sub<M>(x1, mu);
+          if (lane == 0) {
+            sc_mu = mu;
+            sc_s = sv;
+          }
+        } else if (warp == 1) {
+          if (pos) {
+            const md<M> r = w_recip_fast<M>(sigma);
+            if (lane == 0) sc_rsig = r;
+          }
+        } else if (warp == 2) {
+          const md<M> r = w_rsqrt<M>(add<M>(wmul<M>(x1, x1), sigma));
+          if (lane == 0) sc_rmu = r;
         }
       } else if (tid == 0) {
         sc_mu = x1;
@@ -889,53 +898,75 @@ __device__ __forceinline__ void leaf_body(const LeafArgs<M>& a, bool init_bars, 
     __syncthreads();
     LEAF_MARK(l, 5);
     if constexpr (M != 2) {
-      // phase B: thread 0 forms rs = 1/s (the long reciprocal) while warp 1 prepares everything that does
-      // not need it -- x1 > 0: 1/v1 = -s/sigma, u_c = a_jc + g_c/v1, q_c = sigma (1/mu) u_c, so that after
-      // rs only w_c = rs q_c and beta = rs (sigma/mu) remain; x1 <= 0: beta = -v1/mu (v1 = s).
-      if (!deg && tid == 0) sc_rs = recip_fast<M>(sc_s);
-      if (tid >= 32 && tid < 32 + B && !deg) {
-        const int c = tid - 32;
-        const md<M> sv = sc_s, rmu = sc_rmu;
-        if (pos) {
-          const md<M> rv1 = neg(mul<M>(sv, sc_rsig));
-          const md<M> pc = piv[buf][c];
-          const md<M> u = add<M>(pc, mul<M>(rv1, G[c]));
-          const md<M> bq = mul<M>(sigma, rmu);
-          Uc[c] = u;
-          Qc[c] = mul<M>(bq, u);
-          if (c == 0) {
-            sc_rv1 = rv1;
-            sc_bq = bq;
+      static_assert(NT >= 32 * B, "one warp per leaf column");
+      // phase B: warp 0 forms rs = 1/s (the long reciprocal); warps 1..B-1 meanwhile, in two steps (named
+      // barrier 1): x1 > 0: rv1 = 1/v1 = -s/sigma (warp 1), bq = sigma/mu (warp 2), then per column c != l
+      // (warp 1 + slot): u_c = a_jc + g_c/v1 and q_c = bq u_c (c > l), so that after rs only w_c = rs q_c and
+      // beta = rs bq remain; x1 <= 0: bq = -v1/mu = beta (warp 2)
+      const int slot = warp - 1;                               // column slot of warps 1..B-1
+      const int cw = (slot >= 0 && slot < B - 1) ? (slot < l ? slot : slot + 1) : -1;  // its column (!= l)
+      if (!deg) {
+        if (warp == 0) {
+          const md<M> r = w_recip_fast<M>(sc_s);
+          if (lane == 0) sc_rs = r;
+        } else if (warp < B) {
+          const md<M> sv = sc_s, rmu = sc_rmu;
+          if (warp == 1 && pos) {
+            const md<M> r = neg(wmul<M>(sv, sc_rsig));
+            if (lane == 0) sc_rv1 = r;
+          } else if (warp == 2) {
+            const md<M> r = pos ? wmul<M>(sigma, rmu) : neg(wmul<M>(sv, rmu));
+            if (lane == 0) sc_bq = r;
           }
-        } else if (c == 0) {
-          sc_bq = neg(mul<M>(sv, rmu));  // beta itself for x1 <= 0
+          asm volatile("bar.sync 1, %0;" ::"r"(32 * (B - 1)) : "memory");
+          if (pos && cw >= 0) {
+            const md<M> pc = piv[buf][cw];
+            const md<M> u = add<M>(pc, wmul<M>(sc_rv1, G[cw]));
+            const md<M> q = (cw > l) ? wmul<M>(sc_bq, u) : md_zero<M>();
+            if (lane == 0) {
+              Uc[cw] = u;
+              Qc[cw] = q;
+            }
+          }
         }
       }
       __syncthreads();
-      // phase C: beta, u_c / w_c once per column (B threads)
-      if (tid < B) {
-        const int c = tid;
-        const md<M> pc = piv[buf][c];
-        md<M> beta, u, w;
-        if (deg) {
-          beta = md_zero<M>();
-          u = pc;
-          w = md_zero<M>();
+      // phase C: beta and u_c / w_c, one warp per column (warp 0: beta for x1 > 0)
+      if (deg) {
+        if (tid < B) {
+          const int c = tid;
+          if (c < l) SY[c][l] = piv[buf][c];
+          else if (c == l) betas[l] = md_zero<M>();
+          W[c] = md_zero<M>();
           if (c == 0) sc_rv1 = md_from<M>(1.0);
-        } else if (pos) {
-          beta = mul<M>(sc_rs, sc_bq);
-          u = Uc[c];
-          w = mul<M>(sc_rs, Qc[c]);
-        } else {
-          const md<M> rv1 = sc_rs;
-          beta = sc_bq;
-          u = add<M>(pc, mul<M>(rv1, G[c]));
-          w = mul<M>(beta, u);
-          if (c == 0) sc_rv1 = rv1;
         }
-        if (c < l) SY[c][l] = u;
-        else if (c == l) betas[l] = beta;
-        W[c] = (c > l && !deg) ? w : md_zero<M>();
+      } else if (pos) {
+        if (warp == 0) {
+          const md<M> bt = wmul<M>(sc_rs, sc_bq);
+          if (lane == 0) betas[l] = bt;
+        } else if (cw >= 0) {
+          const md<M> w = (cw > l) ? wmul<M>(sc_rs, Qc[cw]) : md_zero<M>();
+          if (lane == 0) {
+            if (cw < l) SY[cw][l] = Uc[cw];
+            W[cw] = w;
+          }
+        }
+        if (tid == 1) W[l] = md_zero<M>();
+      } else {
+        const md<M> rv1 = sc_rs, bt = sc_bq;
+        if (cw >= 0) {
+          const md<M> u = add<M>(piv[buf][cw], wmul<M>(rv1, G[cw]));
+          const md<M> w = (cw > l) ? wmul<M>(bt, u) : md_zero<M>();
+          if (lane == 0) {
+            if (cw < l) SY[cw][l] = u;
+            W[cw] = w;
+          }
+        }
+        if (tid == 0) {
+          betas[l] = bt;
+          sc_rv1 = rv1;
+          W[l] = md_zero<M>();
+        }
       }
       __syncthreads();
     }

@@ -1,5 +1,6 @@
 // kern_misc.cuh -- elementwise md arithmetic and utility kernels.
 #pragma once
+#include "md_warp.cuh"
 #include "types.cuh"
 
 namespace mdls {
@@ -23,6 +24,25 @@ __global__ void md_op_kernel(int op, int64_t n, const double* __restrict__ a, co
       default: r = recip_fast<M>(x); break;
     }
     st<M>(c, ps, e, r);
+  }
+}
+
+// ops 7, 8, 9: the warp-cooperative product / square root / reciprocal (md_warp.cuh), one warp per entry
+template <int M>
+__global__ void md_op_warp_kernel(int op, int64_t n, const double* __restrict__ a, const double* __restrict__ b,
+                                  double* __restrict__ c, int64_t ps) {
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t e = w0; e < n; e += nw) {  // warp-uniform loop
+    const md<M> x = ld<M>(a, ps, e);
+    const md<M> y = (op == 7) ? ld<M>(b, ps, e) : md_zero<M>();
+    md<M> r;
+    if constexpr (M == 2) {
+      r = (op == 7) ? mul<M>(x, y) : (op == 8 ? sqrt_fast<M>(x) : recip_fast<M>(x));
+    } else {
+      r = (op == 7) ? wmul<M>(x, y) : (op == 8 ? w_sqrt_fast<M>(x) : w_recip_fast<M>(x));
+    }
+    if ((threadIdx.x & 31) == 0) st<M>(c, ps, e, r);
   }
 }
 

@@ -253,7 +253,66 @@ int count(int pidx, int op, int64_t M, int64_t K, int64_t nb, mdls_counts* out) 
 
 }  // namespace
 
+namespace mdls {
+
+cudaStream_t capture_begin() {
+  static std::mutex mu;
+  static std::vector<cudaStream_t> cs;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaStream_t st;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (cs.size() <= (size_t)dev) cs.resize((size_t)dev + 1, nullptr);
+    if (!cs[(size_t)dev]) cudaStreamCreateWithFlags(&cs[(size_t)dev], cudaStreamNonBlocking);
+    st = cs[(size_t)dev];
+  }
+  if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return nullptr;
+  return st;
+}
+
+int capture_end(cudaStream_t cs, int64_t launches, void** plan_out) {
+  cudaGraph_t g = nullptr;
+  const cudaError_t e = cudaStreamEndCapture(cs, &g);
+  if (e != cudaSuccess || !g) {
+    if (g) cudaGraphDestroy(g);
+    return MDLS_ERR_CUDA;
+  }
+  cudaGraphExec_t x = nullptr;
+  if (cudaGraphInstantiate(&x, g, 0) != cudaSuccess) {
+    cudaGraphDestroy(g);
+    return MDLS_ERR_CUDA;
+  }
+  auto* p = new PlanImpl;
+  p->graph = g;
+  p->exec = x;
+  cudaGetDevice(&p->device);
+  p->launches = launches;
+  *plan_out = p;
+  return 0;
+}
+
+}  // namespace mdls
+
 extern "C" {
+
+int mdls_plan_launch(void* plan, void* stream) {
+  if (!plan) return -1;
+  auto* p = static_cast<mdls::PlanImpl*>(plan);
+  // the launches are counted like direct calls (the instrumentation's kernels per step)
+  mdls::g_launches.fetch_add(p->launches, std::memory_order_relaxed);
+  return cudaGraphLaunch(p->exec, reinterpret_cast<cudaStream_t>(stream)) == cudaSuccess ? 0 : MDLS_ERR_CUDA;
+}
+
+int64_t mdls_plan_launches(void* plan) { return plan ? static_cast<mdls::PlanImpl*>(plan)->launches : 0; }
+
+void mdls_plan_destroy(void* plan) {
+  if (!plan) return;
+  auto* p = static_cast<mdls::PlanImpl*>(plan);
+  if (p->exec) cudaGraphExecDestroy(p->exec);
+  if (p->graph) cudaGraphDestroy(p->graph);
+  delete p;
+}
 
 const char* mdls_strerror(int code) {
   if (code == 0) return "success";

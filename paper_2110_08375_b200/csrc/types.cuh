@@ -43,6 +43,16 @@ struct StreamGroup {
   ~StreamGroup() { g_stream_group = prev; }
 };
 cudaStream_t side_stream(int which);
+// library-owned CUDA graphs (plans, ledger.cu): capture_begin() returns a private stream of the
+// current device in thread-local capture mode; capture_end() ends the capture and instantiates
+struct PlanImpl {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int device = 0;
+  int64_t launches = 0;  // library kernels per replay
+};
+cudaStream_t capture_begin();
+int capture_end(cudaStream_t cs, int64_t launches, void** plan_out);
 cudaEvent_t pool_event();
 #define MDLS_LAUNCH(FAM, ST, ...)          \
   do {                                     \

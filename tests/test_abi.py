@@ -56,8 +56,29 @@ def test_host_argument_checks(prec):
     assert bs(10, 4, fake, 10, 100, fake, 10, fake, 10, fake, 1 << 20, nul, nul) == -2
     assert bs(8, 4, fake, 8, 64, fake, 4, fake, 8, fake, 1 << 20, nul, nul) == -6          # psy < n
     op = _lib.fn("mdls_md_op_", prec)
-    assert op(9, 10, fake, fake, fake, 10, nul) == -1
+    assert op(10, 10, fake, fake, fake, 10, nul) == -1
     assert op(0, 10, fake, nul, fake, 10, nul) == -4
+    assert op(7, 10, fake, nul, fake, 10, nul) == -4                                       # warp mul needs b
+    bat = _lib.fn("mdls_lstsq_batched_", prec)
+    m = {"dd": 2, "qd": 4, "od": 8}[prec]
+    args = [4, 64, 64, 8, fake, 64, 4096, m * 4096, fake, 64, m * 64, fake, 64, m * 64, 1, 2, fake, 1 << 40, nul, nul]
+    for i, v, rc in ((0, -1, -1), (3, 7, -4), (7, 100, -8), (10, 10, -11), (13, 1, -14), (15, 0, -16), (15, 17, -16),
+                     (17, 10, -18)):
+        bad = list(args)
+        bad[i] = v
+        assert bat(*bad) == rc, (i, v)
+    bws = _lib.fn("mdls_workspace_batched_", prec)
+    assert bws(2, 64, 64, 8, 3) == 3 * (bws(2, 64, 64, 8, 1))
+    assert bws(0, 64, 64, 8, 3) == 0 and bws(2, 64, 64, 8, 0) == 0
+    plan = ctypes.c_void_p(0)
+    lp = _lib.fn("mdls_lstsq_plan_", prec)
+    assert lp(10, 20, 4, fake, 10, 200, fake, 10, fake, 20, 1, fake, 1 << 30, nul, ctypes.byref(plan)) == -1
+    assert plan.value is None
+    bad = list(args[:-1]) + [ctypes.byref(plan)]
+    bad[15] = 0
+    assert _lib.fn("mdls_lstsq_batched_plan_", prec)(*bad) == -16
+    assert _lib.load().mdls_plan_launch(nul, nul) == -1
+    _lib.load().mdls_plan_destroy(nul)
     assert _lib.fn("mdls_workspace_", prec)(0, 10, 20, 4) == 0
     assert _lib.fn("mdls_workspace_", prec)(2, 1024, 1024, 128) > 0
 

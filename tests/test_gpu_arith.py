@@ -83,3 +83,50 @@ def test_fast_sqrt_recip_accuracy(orc, mdls, dev, prec):
         rel = np.abs(d[0]) / np.abs(ref[0])
         print(f"{prec} {op}: max relative difference 2^({np.log2(max(np.max(rel), 1e-300)) + 53 * m:+.2f}) * 2^(-53m)")
         assert np.max(rel) <= 2.0 ** (-53 * m + KARP_BOUND[(prec, op)]), (op, np.max(rel))
+
+
+@pytest.mark.parametrize("prec", ["qd", "od"])
+def test_warp_mul_accuracy(orc, mdls, dev, prec):
+    """The warp-cooperative product (md_warp.cuh: exact limb products split onto a fixed bin grid, summed
+    exactly by a warp butterfly, renormalised) agrees with the oracle's baileyMul_fast product to within
+    2^(-53 m + 2) relative (both are within a few units of 2^(-53 m) of the exact product), including the
+    edge cases of _operands (zeros, equal / opposite operands, 1, 2^-900 and 2^600 -- the last two take the
+    sequential fallback), and its result is renormalised (|limb k+1| <= ulp(limb k))."""
+    m = inputs.limbs(prec)
+    n = {"qd": 20000, "od": 6000}[prec]
+    a, b = _operands(prec, n, 29)
+    ga, gb = torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev)
+    got = mdls.md_op("wmul", prec, ga, gb).cpu().numpy()
+    ref = orc.md_op("mul", prec, a, b)
+    d = orc.md_op("sub", prec, got, ref)
+    nz = ref[0] != 0
+    assert np.all(got[:, ~nz] == 0.0)
+    rel = np.abs(d[0][nz]) / np.abs(ref[0][nz])
+    print(f"{prec} wmul: max relative difference 2^({np.log2(max(np.max(rel), 1e-300)) + 53 * m:+.2f}) * 2^(-53m)")
+    assert np.max(rel) <= 2.0 ** (-53 * m + 2)
+    for k in range(m - 1):
+        hi, lo = np.abs(got[k]), np.abs(got[k + 1])
+        assert np.all(lo <= np.spacing(hi) + 0.0), k
+
+
+@pytest.mark.parametrize("prec", ["qd", "od"])
+def test_warp_sqrt_recip_accuracy(orc, mdls, dev, prec):
+    """The warp versions of the panel's Newton/Karp sqrt and reciprocal meet the same bounds as the
+    per-thread ones (KARP_BOUND, vs the oracle's QDlib-style sqrt and long division)."""
+    m = inputs.limbs(prec)
+    n = 6000
+    a, _ = _operands(prec, n, 31)
+    a = np.where(a[0] < 0, -a, a)
+    z = a[0] == 0
+    a[:, z] = 0.0
+    a[0, z] = 1.0
+    ga = torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    one = np.zeros_like(a)
+    one[0] = 1.0
+    for op, base, ref in (("wsqrt_fast", "sqrt_fast", orc.md_op("sqrt", prec, a)),
+                          ("wrecip_fast", "recip_fast", orc.md_op("div", prec, one, a))):
+        got = mdls.md_op(op, prec, ga).cpu().numpy()
+        d = orc.md_op("sub", prec, got, ref)
+        rel = np.abs(d[0]) / np.abs(ref[0])
+        print(f"{prec} {op}: max relative difference 2^({np.log2(max(np.max(rel), 1e-300)) + 53 * m:+.2f}) * 2^(-53m)")
+        assert np.max(rel) <= 2.0 ** (-53 * m + KARP_BOUND[(prec, base)])

@@ -9,6 +9,7 @@
 
 namespace mdls {
 void set_stage(int) {}
+int max_cluster_size() { return 16; }
 void trace_begin(cudaStream_t, int) {}
 void trace_end(cudaStream_t, int) {}
 }  // namespace mdls
