@@ -703,6 +703,32 @@ __device__ __forceinline__ void leaf_t_column(md<M> (&Ts)[BT][BT], const md<M> (
   Ts[r][ll] = neg(mul<M>(betas[ll], acc.get()));
 }
 
+// the same column with the <= BT-1 terms of a row spread over lanes (one product each, merged by a shuffle tree)
+// and the scaling by -beta_ll taken by the warp: the octo double version (a row's sequential sum of up to seven
+// od products is ~5k cycles per term)
+template <int M, int BT>
+__device__ __forceinline__ void leaf_t_column_warp(md<M> (&Ts)[BT][BT], const md<M> (&SY)[BT][BT],
+                                                   const md<M> (&betas)[BT], int ll, int rank, int C, int lane) {
+  static_assert(BT <= 32, "one lane per term");
+  for (int r = rank; r < ll; r += C) {  // warp-uniform
+    const int p = r + lane;
+    Acc<M> acc;
+    acc.init();
+    if (p < ll) acc.add_prod(Ts[r][p], SY[p][ll]);
+#pragma unroll
+    for (int d = BT / 2; d >= 1; d >>= 1) {
+      Acc<M> o = acc_shfl_down<M>(acc, d);
+      if (lane + d < BT) acc.merge(o);
+    }
+    md<M> sum = acc.get();
+#pragma unroll
+    for (int k = 0; k < M; ++k) sum.v[k] = __shfl_sync(0xffffffffu, sum.v[k], 0);
+    const md<M> t = neg(wmul_any<M>(betas[ll], sum));
+    if (lane == 0) Ts[r][ll] = t;
+  }
+  if (lane == 0 && ll % C == rank) Ts[ll][ll] = betas[ll];
+}
+
 // One leaf (the body of leaf_reg_kernel; leaf_chain_kernel runs it for every leaf of the
 // factorisation).  init_bars: initialise the column mbarriers (first leaf of the kernel);
 // zinit / zpar: initialise the prologue mbarriers / their phase parity for this leaf.
@@ -871,11 +897,12 @@ __device__ __forceinline__ void leaf_body(const LeafArgs<M>& a, bool init_bars, 
         }
       }
     } else {
-      // qd/od, phase A: every md product of the scalar chain is taken by a whole warp (md_warp.cuh):
+      // qd/od, phase A: every md product of the scalar chain is computed by a whole warp (od: warp-cooperative,
+      // md_warp.cuh; qd: redundantly per lane):
       // warp 0: mu = sqrt(x1^2 + sigma), s = x1 +- mu; warp 1: 1/sigma (x1 > 0); warp 2: 1/mu = rsqrt(x1^2 + sigma)
       if (!deg) {
         if (warp == 0) {
-          const md<M> mu = w_sqrt_fast<M>(add<M>(wmul<M>(x1, x1), sigma));
+          const md<M> mu = w_sqrt_fast<M>(add<M>(wmul_any<M>(x1, x1), sigma));
           const md<M> sv = pos ? add<M>(x1, mu) : sub<M>(x1, mu);
           if (lane == 0) {
             sc_mu = mu;
@@ -887,14 +914,17 @@ __device__ __forceinline__ void leaf_body(const LeafArgs<M>& a, bool init_bars, 
             if (lane == 0) sc_rsig = r;
           }
         } else if (warp == 2) {
-          const md<M> r = w_rsqrt<M>(add<M>(wmul<M>(x1, x1), sigma));
+          const md<M> r = w_rsqrt<M>(add<M>(wmul_any<M>(x1, x1), sigma));
           if (lane == 0) sc_rmu = r;
         }
       } else if (tid == 0) {
         sc_mu = x1;
       }
     }
-    if (warp == 3 && l > 0) leaf_t_column<M>(Ts, SY, betas, l - 1, rank, C, lane);  // this CTA's rows of T(:, l-1)
+    if (warp == 3 && l > 0) {
+      if constexpr (M == 8) leaf_t_column_warp<M>(Ts, SY, betas, l - 1, rank, C, lane);
+      else leaf_t_column<M>(Ts, SY, betas, l - 1, rank, C, lane);
+    }  // this CTA's rows of T(:, l-1)
     __syncthreads();
     LEAF_MARK(l, 5);
     if constexpr (M != 2) {
@@ -912,17 +942,17 @@ __device__ __forceinline__ void leaf_body(const LeafArgs<M>& a, bool init_bars, 
         } else if (warp < B) {
           const md<M> sv = sc_s, rmu = sc_rmu;
           if (warp == 1 && pos) {
-            const md<M> r = neg(wmul<M>(sv, sc_rsig));
+            const md<M> r = neg(wmul_any<M>(sv, sc_rsig));
             if (lane == 0) sc_rv1 = r;
           } else if (warp == 2) {
-            const md<M> r = pos ? wmul<M>(sigma, rmu) : neg(wmul<M>(sv, rmu));
+            const md<M> r = pos ? wmul_any<M>(sigma, rmu) : neg(wmul_any<M>(sv, rmu));
             if (lane == 0) sc_bq = r;
           }
           asm volatile("bar.sync 1, %0;" ::"r"(32 * (B - 1)) : "memory");
           if (pos && cw >= 0) {
             const md<M> pc = piv[buf][cw];
-            const md<M> u = add<M>(pc, wmul<M>(sc_rv1, G[cw]));
-            const md<M> q = (cw > l) ? wmul<M>(sc_bq, u) : md_zero<M>();
+            const md<M> u = add<M>(pc, wmul_any<M>(sc_rv1, G[cw]));
+            const md<M> q = (cw > l) ? wmul_any<M>(sc_bq, u) : md_zero<M>();
             if (lane == 0) {
               Uc[cw] = u;
               Qc[cw] = q;
@@ -942,10 +972,10 @@ __device__ __forceinline__ void leaf_body(const LeafArgs<M>& a, bool init_bars, 
         }
       } else if (pos) {
         if (warp == 0) {
-          const md<M> bt = wmul<M>(sc_rs, sc_bq);
+          const md<M> bt = wmul_any<M>(sc_rs, sc_bq);
           if (lane == 0) betas[l] = bt;
         } else if (cw >= 0) {
-          const md<M> w = (cw > l) ? wmul<M>(sc_rs, Qc[cw]) : md_zero<M>();
+          const md<M> w = (cw > l) ? wmul_any<M>(sc_rs, Qc[cw]) : md_zero<M>();
           if (lane == 0) {
             if (cw < l) SY[cw][l] = Uc[cw];
             W[cw] = w;
@@ -955,8 +985,8 @@ __device__ __forceinline__ void leaf_body(const LeafArgs<M>& a, bool init_bars, 
       } else {
         const md<M> rv1 = sc_rs, bt = sc_bq;
         if (cw >= 0) {
-          const md<M> u = add<M>(piv[buf][cw], wmul<M>(rv1, G[cw]));
-          const md<M> w = (cw > l) ? wmul<M>(bt, u) : md_zero<M>();
+          const md<M> u = add<M>(piv[buf][cw], wmul_any<M>(rv1, G[cw]));
+          const md<M> w = (cw > l) ? wmul_any<M>(bt, u) : md_zero<M>();
           if (lane == 0) {
             if (cw < l) SY[cw][l] = u;
             W[cw] = w;
@@ -996,7 +1026,10 @@ __device__ __forceinline__ void leaf_body(const LeafArgs<M>& a, bool init_bars, 
 
   // ---- last T column, write-back of R/v, explicit Y, beta, T ----
   __syncthreads();
-  if (warp == 3) leaf_t_column<M>(Ts, SY, betas, B - 1, rank, C, lane);
+  if (warp == 3) {
+    if constexpr (M == 8) leaf_t_column_warp<M>(Ts, SY, betas, B - 1, rank, C, lane);
+    else leaf_t_column<M>(Ts, SY, betas, B - 1, rank, C, lane);
+  }
   if (valid) {
 #pragma unroll
     for (int q = 0; q < V; ++q) {

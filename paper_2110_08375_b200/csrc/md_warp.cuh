@@ -143,11 +143,13 @@ __device__ __noinline__ md<M> wmul(const md<M>& a, const md<M>& b) {
   return r;
 }
 
-// dispatch: double double stays per thread (a dd product is a handful of FP64 operations)
+// dispatch: only the octo double product is faster across the warp (B200, tools/wmul_lat.cu: one dependent
+// od product 4.3k cycles by the warp vs 6.7k by one thread; qd 1.9k vs 0.9k), so dd and qd stay per thread
+// (every lane computes the same product)
 template <int M>
 __device__ __forceinline__ md<M> wmul_any(const md<M>& a, const md<M>& b) {
-  if constexpr (M == 2) return dd_mul(a, b);
-  else return wmul<M>(a, b);
+  if constexpr (M == 8) return wmul<M>(a, b);
+  else return mul<M>(a, b);
 }
 
 // the latency-lean square root / reciprocal / reciprocal square root of md.cuh with every product of
@@ -179,8 +181,8 @@ __device__ __forceinline__ md<M> w_sqrt_fast(const md<M>& a) {
   constexpr int H = M / 2;
   const md<H> yh = w_rsqrt_to<H, M>(a);
   const md<M> y = md_trunc<M, H>(yh);
-  const md<M> x = wmul<M>(a, y);
-  const md<M> r = add<M>(a, neg(wmul<M>(x, x)));
+  const md<M> x = wmul_any<M>(a, y);
+  const md<M> r = add<M>(a, neg(wmul_any<M>(x, x)));
   const md<H> c = wmul_any<H>(md_trunc<H, M>(r), scale_pow2<H>(yh, 0.5));
   return add<M>(x, md_trunc<M, H>(c));
 }
@@ -197,7 +199,7 @@ __device__ __forceinline__ md<M> w_recip_fast(const md<M>& d) {
   if constexpr (H >= 2) yh = md_trunc<H, 2>(recip_step<2>(md_trunc<2, M>(d), md_trunc<2, H>(yh)));
   if constexpr (H >= 4) yh = md_trunc<H, 4>(w_recip_step<4>(md_trunc<4, M>(d), md_trunc<4, H>(yh)));
   const md<M> y = md_trunc<M, H>(yh);
-  const md<M> e = add<M>(md_from<M>(1.0), neg(wmul<M>(d, y)));
+  const md<M> e = add<M>(md_from<M>(1.0), neg(wmul_any<M>(d, y)));
   const md<H> c = wmul_any<H>(yh, md_trunc<H, M>(e));
   return add<M>(y, md_trunc<M, H>(c));
 }
