@@ -263,16 +263,6 @@ def run_ours(args, ws, rank, local):
         ms = [a.elapsed_time(bb) for a, bb in ev]
         ms_step = max_over_ranks(sum(ms) / steps)
         out = {"ms_per_step": ms_step, "ms_min": min(ms), "launches_per_step": per_step_launches}
-        if with_trace:  # second pass, traced launch by launch (per-stage and per-family kernel times)
-            mdls.trace_enable(True)
-            for i in range(steps):
-                flush.fill_(float(i))
-                mdls.lstsq(prec, A, b, nb, form_q=True, work=work)
-            torch.cuda.synchronize()
-            mdls.trace_enable(False)
-            tr = mdls.trace_collect()
-            out["trace"] = {k: ({s: v / steps for s, v in d.items()} if isinstance(d, dict) else d / steps)
-                            for k, d in tr.items()}
         if with_e2e:  # through the public API from pinned host buffers, copies inside the timed region
             A_p = torch.from_numpy(A_h).pin_memory()
             b_p = torch.from_numpy(b_h).pin_memory()
@@ -307,6 +297,16 @@ def run_ours(args, ws, rank, local):
             out["d2h"] = x_p.numel() * 8
             # parity guard on the e2e result (cheap invariant: finite, dev_info 0)
             assert int(info.item()) == 0 and bool(np.isfinite(x_p.numpy()).all())
+        if with_trace:  # second pass, traced launch by launch (per-stage and per-family kernel times)
+            mdls.trace_enable(True)
+            for i in range(steps):
+                flush.fill_(float(i))
+                mdls.lstsq(prec, A, b, nb, form_q=True, work=work)
+            torch.cuda.synchronize()
+            mdls.trace_enable(False)
+            tr = mdls.trace_collect()
+            out["trace"] = {k: ({s: v / steps for s, v in d.items()} if isinstance(d, dict) else d / steps)
+                            for k, d in tr.items()}
         del plan
         return out
 

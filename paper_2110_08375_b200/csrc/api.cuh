@@ -146,7 +146,7 @@ static QrBufs<M> qr_bufs(void* work, const Plan& p, int64_t Mr, int64_t K, int64
   const int64_t mx = std::max(Mr, K);
   b.X = Mat{at<double>(work, p.x), nb, nb * mx};
   b.part = at<double>(work, p.part);
-  b.part_cap = kMaxSplit * nb * mx;
+  b.part_cap = lane_part_elems<M>(nb, mx);
   b.xbase = b.X.p;
   b.pbase = b.part;
   b.xcap = nb * mx;

@@ -66,105 +66,169 @@ __global__ void __launch_bounds__(GemmTile<M, V>::NT) gemm_kernel(GemmArgs g) {
   // consecutive lanes own consecutive output ROWS: the epilogue's C loads/stores and the split-K
   // partial stores are coalesced along the column-major planes (they dominate when k is small)
   const int ty = tid % NY, tx = tid / NY;
-  // work items (column tile fastest, then row tile, then split) in a grid-stride loop: one item per
-  // CTA normally; a capped grid (GemmCap) keeps a low-priority product to part of the device
   const int64_t ntx = (g.n + BN - 1) / BN, nty = (g.m + BM - 1) / BM;
-  const int64_t nitems = ntx * nty * g.S;
-  for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
-  const int64_t z = item / (ntx * nty);
-  const int64_t i0 = ((item / ntx) % nty) * BM, j0 = (item % ntx) * BN;
-  const int64_t kb = z * g.kc;
-  const int64_t ke = min(g.k, kb + g.kc);
-  const int nkt = (int)((ke - kb + BK - 1) / BK);
 
-  // issue the copies of k-tile t into stage t % STAGES (consecutive threads walk the contiguous
-  // direction of each operand: coalesced global reads)
-  auto load_tile = [&](int t) {
-    const int stg = t % STAGES;
-    const int64_t k0 = kb + (int64_t)t * BK;
-    double* as = As + stg * Sm::A_ST;
-    double* bs = Bs + stg * Sm::B_ST;
-    for (int e = tid; e < BM * BK; e += NT) {
-      int ii, kk;
-      if (TA) { kk = e % BK; ii = e / BK; } else { ii = e % BM; kk = e / BM; }
-      const int64_t gi = i0 + ii, gk = k0 + kk;
-      const bool ok = gi < g.m && gk < ke;
-      const int64_t off = ok ? (TA ? (gk + gi * g.lda) : (gi + gk * g.lda)) : 0;
+  // the k-tiles [kb, ke) of the output tile (i0, j0) into acc, through the cp.async stage ring
+  auto run_tile = [&](int64_t i0, int64_t j0, int64_t kb, int64_t ke, Acc<M> (&acc)[TM][TN]) {
+    const int nkt = (int)((ke - kb + BK - 1) / BK);
+    // issue the copies of k-tile t into stage t % STAGES (consecutive threads walk the contiguous
+    // direction of each operand: coalesced global reads)
+    auto load_tile = [&](int t) {
+      const int stg = t % STAGES;
+      const int64_t k0 = kb + (int64_t)t * BK;
+      double* as = As + stg * Sm::A_ST;
+      double* bs = Bs + stg * Sm::B_ST;
+      for (int e = tid; e < BM * BK; e += NT) {
+        int ii, kk;
+        if (TA) { kk = e % BK; ii = e / BK; } else { ii = e % BM; kk = e / BM; }
+        const int64_t gi = i0 + ii, gk = k0 + kk;
+        const bool ok = gi < g.m && gk < ke;
+        const int64_t off = ok ? (TA ? (gk + gi * g.lda) : (gi + gk * g.lda)) : 0;
 #pragma unroll
-      for (int l = 0; l < M; ++l) cp_async8(as + (l * BK + kk) * BMP + ii, g.A + l * g.psa + off, ok);
+        for (int l = 0; l < M; ++l) cp_async8(as + (l * BK + kk) * BMP + ii, g.A + l * g.psa + off, ok);
+      }
+      for (int e = tid; e < BK * BN; e += NT) {
+        int kk, jj;
+        if (TB) { jj = e % BN; kk = e / BN; } else { kk = e % BK; jj = e / BK; }
+        const int64_t gj = j0 + jj, gk = k0 + kk;
+        const bool ok = gj < g.n && gk < ke;
+        const int64_t off = ok ? (TB ? (gj + gk * g.ldb) : (gk + gj * g.ldb)) : 0;
+#pragma unroll
+        for (int l = 0; l < M; ++l) cp_async8(bs + (l * BK + kk) * BNP + jj, g.B + l * g.psb + off, ok);
+      }
+    };
+#pragma unroll
+    for (int t = 0; t < TM; ++t)
+#pragma unroll
+      for (int u = 0; u < TN; ++u) acc[t][u].init();
+#pragma unroll
+    for (int t = 0; t < STAGES - 1; ++t) {
+      if (t < nkt) load_tile(t);
+      cp_async_commit();  // one group per tile slot, empty past the end (keeps the wait counts uniform)
     }
-    for (int e = tid; e < BK * BN; e += NT) {
-      int kk, jj;
-      if (TB) { jj = e % BN; kk = e / BN; } else { kk = e % BK; jj = e / BK; }
-      const int64_t gj = j0 + jj, gk = k0 + kk;
-      const bool ok = gj < g.n && gk < ke;
-      const int64_t off = ok ? (TB ? (gj + gk * g.ldb) : (gk + gj * g.ldb)) : 0;
+    for (int t = 0; t < nkt; ++t) {
+      cp_async_wait<STAGES - 2>();  // this thread's copies of tile t have landed
+      __syncthreads();              // everyone's have; and everyone finished computing tile t-1
+      if (t + STAGES - 1 < nkt) load_tile(t + STAGES - 1);  // refill the stage tile t-1 used
+      cp_async_commit();
+      const double* as = As + (t % STAGES) * Sm::A_ST;
+      const double* bs = Bs + (t % STAGES) * Sm::B_ST;
+#pragma unroll 2
+      for (int kk = 0; kk < BK; ++kk) {
+        md<M> a[TM], b[TN];
 #pragma unroll
-      for (int l = 0; l < M; ++l) cp_async8(bs + (l * BK + kk) * BNP + jj, g.B + l * g.psb + off, ok);
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+          for (int l = 0; l < M; ++l) a[i].v[l] = as[(l * BK + kk) * BMP + ty + i * NY];
+#pragma unroll
+        for (int u = 0; u < TN; ++u)
+#pragma unroll
+          for (int l = 0; l < M; ++l) b[u].v[l] = bs[(l * BK + kk) * BNP + tx + u * NX];
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+          for (int u = 0; u < TN; ++u) acc[i][u].add_prod(a[i], b[u]);
+      }
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int u = 0; u < TN; ++u) acc[i][u].renorm_bins();
+    }
+    cp_async_wait<0>();
+    __syncthreads();  // every thread done with the stages before the next tile refills them
+  };
+
+  // C (mode)= acc, or the split-K partial z
+  auto epilogue = [&](int64_t i0, int64_t j0, int64_t z, Acc<M> (&acc)[TM][TN]) {
+#pragma unroll
+    for (int t = 0; t < TM; ++t) {
+      const int64_t gi = i0 + ty + t * NY;
+      if (gi >= g.m) continue;
+#pragma unroll
+      for (int u = 0; u < TN; ++u) {
+        const int64_t gj = j0 + tx + u * NX;
+        if (gj >= g.n) continue;
+        if (g.part) {
+          const int64_t pps = g.m * g.n * g.S;
+          st<M>(g.part, pps, gi + (gj + z * g.n) * g.m, acc[t][u].get());
+        } else {
+          const int64_t e = gi + gj * g.ldc;
+          md<M> c = (g.mode == 1 || g.mode == 2) ? ld<M>(g.C, g.psc, e) : md_zero<M>();
+          st<M>(g.C, g.psc, e, apply_mode<M>(g.mode, c, acc[t][u].get()));
+        }
+      }
     }
   };
 
   Acc<M> acc[TM][TN];
-#pragma unroll
-  for (int t = 0; t < TM; ++t)
-#pragma unroll
-    for (int u = 0; u < TN; ++u) acc[t][u].init();
-
-#pragma unroll
-  for (int t = 0; t < STAGES - 1; ++t) {
-    if (t < nkt) load_tile(t);
-    cp_async_commit();  // one group per tile slot, empty past the end (keeps the wait counts uniform)
-  }
-  for (int t = 0; t < nkt; ++t) {
-    cp_async_wait<STAGES - 2>();  // this thread's copies of tile t have landed
-    __syncthreads();              // everyone's have; and everyone finished computing tile t-1
-    if (t + STAGES - 1 < nkt) load_tile(t + STAGES - 1);  // refill the stage tile t-1 used
-    cp_async_commit();
-    const double* as = As + (t % STAGES) * Sm::A_ST;
-    const double* bs = Bs + (t % STAGES) * Sm::B_ST;
-#pragma unroll 2
-    for (int kk = 0; kk < BK; ++kk) {
-      md<M> a[TM], b[TN];
-#pragma unroll
-      for (int i = 0; i < TM; ++i)
-#pragma unroll
-        for (int l = 0; l < M; ++l) a[i].v[l] = as[(l * BK + kk) * BMP + ty + i * NY];
-#pragma unroll
-      for (int u = 0; u < TN; ++u)
-#pragma unroll
-        for (int l = 0; l < M; ++l) b[u].v[l] = bs[(l * BK + kk) * BNP + tx + u * NX];
-#pragma unroll
-      for (int i = 0; i < TM; ++i)
-#pragma unroll
-        for (int u = 0; u < TN; ++u) acc[i][u].add_prod(a[i], b[u]);
+  if (g.sk_w == 0) {
+    // work items (column tile fastest, then row tile, then split) in a grid-stride loop: one item per
+    // CTA normally; a capped grid (GemmCap) keeps a low-priority product to part of the device
+    const int64_t nitems = ntx * nty * g.S;
+    for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
+      const int64_t z = item / (ntx * nty);
+      const int64_t i0 = ((item / ntx) % nty) * BM, j0 = (item % ntx) * BN;
+      const int64_t kb = z * g.kc;
+      run_tile(i0, j0, kb, min(g.k, kb + g.kc), acc);
+      epilogue(i0, j0, z, acc);
     }
-#pragma unroll
-    for (int i = 0; i < TM; ++i)
-#pragma unroll
-      for (int u = 0; u < TN; ++u) acc[i][u].renorm_bins();
+    return;
   }
-  cp_async_wait<0>();
-
-  // ---- epilogue ----
+  // stream-K: this CTA's contiguous range of the tile-major iteration space, taken from its END: the last
+  // segment (the head of a tile finished by a later CTA) is published first, and the first segment (the
+  // tail of a tile started by earlier CTAs, which published their parts first) is finished last -- so no
+  // CTA ever waits for more than the first segment of its predecessors
+  constexpr int RS = TM * TN * Acc<M>::NV;  // partial doubles per thread
+  const int64_t I = g.sk_I, W = g.sk_w, total = ntx * nty * I;
+  const int64_t p = blockIdx.x;
+  const int64_t beg = p * W;
+  int64_t hi = min(total, beg + W);
+  while (hi > beg) {
+    const int64_t tile = (hi - 1) / I;
+    const int64_t lo = max(beg, tile * I);
+    const int64_t kf = lo - tile * I, kl = hi - tile * I;
+    const int64_t i0 = ((tile / ntx) % nty) * BM, j0 = (tile % ntx) * BN;
+    run_tile(i0, j0, kf * BK, min(g.k, kl * BK), acc);
+    if (kf == 0 && kl == I) {
+      epilogue(i0, j0, 0, acc);
+    } else if (kl < I) {
+      // not the tile's last k-tile: publish the partial (slot p; only a CTA's last segment can be partial)
+      double* slot = g.sk_part + p * (int64_t)RS * NT;
 #pragma unroll
-  for (int t = 0; t < TM; ++t) {
-    const int64_t gi = i0 + ty + t * NY;
-    if (gi >= g.m) continue;
+      for (int t = 0; t < TM; ++t)
 #pragma unroll
-    for (int u = 0; u < TN; ++u) {
-      const int64_t gj = j0 + tx + u * NX;
-      if (gj >= g.n) continue;
-      if (g.part) {
-        const int64_t pps = g.m * g.n * g.S;
-        st<M>(g.part, pps, gi + (gj + z * g.n) * g.m, acc[t][u].get());
-      } else {
-        const int64_t e = gi + gj * g.ldc;
-        md<M> c = (g.mode == 1 || g.mode == 2) ? ld<M>(g.C, g.psc, e) : md_zero<M>();
-        st<M>(g.C, g.psc, e, apply_mode<M>(g.mode, c, acc[t][u].get()));
+        for (int u = 0; u < TN; ++u)
+#pragma unroll
+          for (int v = 0; v < Acc<M>::NV; ++v) __stcg(slot + ((t * TN + u) * Acc<M>::NV + v) * NT + tid, acc[t][u].r(v));
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) atomicAdd(g.sk_flags + tile, 1);
+    } else {
+      // the tile's last k-tile: wait for the earlier segments (CTAs pf..p-1), merge their partials into this
+      // CTA's part in CTA order (fixed: bitwise reproducible)
+      const int64_t pf = (tile * I) / W;
+      const int need = (int)(p - pf);
+      if (tid == 0) {
+        volatile int* f = g.sk_flags + tile;
+        while (*f < need) __nanosleep(32);
+        __threadfence();
       }
+      __syncthreads();
+      for (int64_t q = pf; q < p; ++q) {
+        const double* slot = g.sk_part + q * (int64_t)RS * NT;
+#pragma unroll
+        for (int t = 0; t < TM; ++t)
+#pragma unroll
+          for (int u = 0; u < TN; ++u) {
+            Acc<M> o;
+#pragma unroll
+            for (int v = 0; v < Acc<M>::NV; ++v) o.r(v) = __ldcg(slot + ((t * TN + u) * Acc<M>::NV + v) * NT + tid);
+            acc[t][u].merge(o);
+          }
+      }
+      epilogue(i0, j0, 0, acc);
     }
-  }
-  if (item + gridDim.x < nitems) __syncthreads();  // every thread done with the stages before the refill
+    hi = lo;
   }
 }
 
@@ -265,6 +329,30 @@ void gemm_launch(cudaStream_t st, int64_t m, int64_t n, int64_t k, CMat A, CMat 
   int64_t kc = cdiv(cdiv(k, S), Tl::BK) * Tl::BK;
   S = std::max<int64_t>(1, cdiv(k, kc));
   GemmArgs g{m, n, k, A.p, A.ld, A.ps, B.p, B.ld, B.ps, C.p, C.ld, C.ps, mode, kc, S > 1 ? part : nullptr, S};
+  // stream-K for a product of one or two waves of tiles (no split): the tiles x k-tiles iteration space is
+  // cut into equal contiguous ranges, one per resident CTA slot, so every SM holds the same work
+  // (256 tiles of 64 x 64 on 296 dd slots leave 40 SMs with one CTA otherwise)
+  static const bool sk_on = [] {
+    const char* v = getenv("MDLS_STREAMK");
+    return !(v && v[0] == '0');
+  }();
+  if (sk_on && S == 1 && part && kt >= 2 && tiles <= 2 * slots && tiles % slots != 0 && tiles * kt >= slots) {
+    const int64_t units = tiles * kt;
+    const int64_t W = cdiv(units, slots), P = cdiv(units, W);
+    constexpr int64_t RS = (int64_t)Tl::TM * Tl::TN * Acc<M>::NV * Tl::NT;  // partial doubles per CTA
+    const int64_t flag_d = cdiv(tiles * (int64_t)sizeof(int), (int64_t)sizeof(double));
+    if ((flag_d + P * RS) <= part_cap_elems * M) {
+      g.sk_w = W;
+      g.sk_I = kt;
+      g.sk_flags = reinterpret_cast<int*>(part);
+      g.sk_part = part + flag_d;
+      cudaMemsetAsync(g.sk_flags, 0, (size_t)tiles * sizeof(int), st);
+      gemm_set_attr<M, V, TA, TB>();
+      MDLS_LAUNCH(F_GEMM, st,
+                  gemm_kernel<M, V, TA, TB><<<(unsigned)P, Tl::NT, GemmSmem<M, V, TA, TB>::bytes, st>>>(g));
+      return;
+    }
+  }
   gemm_kernel_launch<M, V, TA, TB>(st, g);
   if (S > 1)
     MDLS_LAUNCH(F_GEMM, st, splitk_reduce_kernel<M><<<grid_for(m * n, 256), 256, 0, st>>>(m, n, S, part, C.p, C.ld, C.ps, mode));

@@ -28,6 +28,13 @@ struct Plan {
          info = 0, total = 0;
 };
 
+// md elements of one lane's split-K / stream-K partial buffer: kMaxSplit nb x max(M, K) partials, or the
+// stream-K partials of two CTAs per SM (<= 64 x 64 dd / 32 x 32 qd / 32 x 16 od tiles: 8192 doubles) + flags
+template <int M>
+int64_t lane_part_elems(int64_t nb, int64_t mx) {
+  return std::max<int64_t>(kMaxSplit * nb * mx, (int64_t)(2 * num_sms() + 8) * 8192 / M + 4096);
+}
+
 template <int M>
 Plan make_plan(int op, int64_t Mr, int64_t K, int64_t nb) {
   Plan p;
@@ -52,7 +59,7 @@ Plan make_plan(int op, int64_t Mr, int64_t K, int64_t nb) {
   if (op == MDLS_OP_APPLY_QT) p.y = take(md * Mr * K);
   if (qr_like || op == MDLS_OP_APPLY_QT) {
     p.x = take(5 * md * nb * mx);  // one GEMM-intermediate buffer per stream lane
-    p.part = take(5 * md * kMaxSplit * nb * mx);
+    p.part = take(5 * md * lane_part_elems<M>(nb, mx));
   }
   p.v0 = take(md * mx);
   p.v1 = take(md * mx);

@@ -154,6 +154,12 @@ struct GemmArgs {
   int64_t kc;     // k chunk per split
   double* part;   // split partials (nullptr: no split)
   int64_t S;      // number of splits
+  // stream-K (sk_w > 0): CTA p computes the k-iterations [p*sk_w, (p+1)*sk_w) of the tile-major iteration
+  // space (tiles x sk_I k-tiles); a tile split over CTAs is finished by the CTA holding its last k-tile,
+  // which merges the others' partials (sk_part, one slot per CTA) in k order after their flags
+  int64_t sk_w = 0, sk_I = 0;
+  int* sk_flags = nullptr;
+  double* sk_part = nullptr;
 };
 
 

@@ -70,3 +70,28 @@ def test_gemm_argument_errors(mdls, dev):
     assert f(-1, 4, 4, 0, 0, p, 4, 16, p, 4, 16, p, 4, 16, 0, None, 0, None) == -1
     assert f(4, 4, 4, 2, 0, p, 4, 16, p, 4, 16, p, 4, 16, 0, None, 0, None) == -4
     assert f(4, 4, 4, 0, 0, p, 4, 16, p, 4, 16, p, 4, 16, 0, None, 0, None) == -12  # C aliases A
+
+
+@pytest.mark.parametrize("prec,m,n,k,tb", [("dd", 1024, 1024, 128, 1), ("dd", 600, 700, 300, 0), ("qd", 512, 640, 128, 1),
+                                           ("od", 256, 480, 96, 0)])
+def test_gemm_stream_k(orc, mdls, dev, prec, m, n, k, tb):
+    """One- and two-wave shapes take the stream-K path (tiles x k-tiles split evenly over the CTA slots, a tile's
+    last CTA merging the others' partials in k order): sampled entries vs the oracle dots, and the result is
+    bitwise identical run to run (fixed segmentation, fixed merge order)."""
+    A = inputs.random_matrix(m, k, prec, seed=m + k)
+    B = inputs.random_matrix(n if tb else k, k if tb else n, prec, seed=n + k)
+    C0 = inputs.random_matrix(m, n, prec, seed=7)
+    outs = []
+    for _ in range(2):
+        outs.append(mdls.gemm(prec, _gpu(A, dev), _gpu(B, dev), C=_gpu(C0, dev).clone(), trans_b=bool(tb), mode=1))
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])
+    Cg = outs[0].cpu().numpy()
+    Bop = _op(B, tb)
+    rng = np.random.default_rng(3)
+    for i, j in zip(rng.integers(0, m, 40), rng.integers(0, n, 40)):
+        p = orc.dot(prec, np.ascontiguousarray(A.transpose(0, 2, 1)[:, i, :]), np.ascontiguousarray(Bop[:, :, j]))
+        ref = orc.md_op("add", prec, C0[:, j, i][:, None], p[:, None])[:, 0]
+        d = orc.md_op("sub", prec, Cg[:, j, i][:, None], ref[:, None])[0, 0]
+        scale = float(np.sum(np.abs(A[0, :, i] * Bop[0, :, j]))) + abs(float(C0[0, j, i]))
+        assert abs(d) <= 1e3 * k * U_OF[prec] * scale, (i, j, d)
