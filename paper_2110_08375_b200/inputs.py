@@ -135,3 +135,22 @@ def random_vector_torch(n: int, prec, seed: int, device="cuda"):
         ulp = torch.nextafter(prev, torch.full_like(prev, float("inf"))) - prev
         out[k] = (torch.rand(n, generator=g, dtype=torch.float64, device=device) * 2.0 - 1.0) * ulp * 0.5
     return out
+
+
+def random_matrix_torch(rows: int, cols: int, prec, seed: int, device="cuda"):
+    """Large-size variant of random_matrix generated on the device (seeded torch Philox): (m, cols, rows),
+    limb 0 uniform in [-1, 1), limb k = u * ulp(limb k-1) / 2 with u uniform in (-1, 1)."""
+    import torch
+
+    m = limbs(prec)
+    g = torch.Generator(device=device)
+    g.manual_seed(int(seed) + 104729)
+    out = torch.empty((m, cols, rows), dtype=torch.float64, device=device)
+    out[0] = torch.rand((cols, rows), generator=g, dtype=torch.float64, device=device) * 2.0 - 1.0
+    for k in range(1, m):
+        prev = out[k - 1].abs()
+        ulp = torch.nextafter(prev, torch.full_like(prev, float("inf"))) - prev
+        r = torch.rand((cols, rows), generator=g, dtype=torch.float64, device=device) * 2.0 - 1.0
+        out[k] = torch.where(out[k - 1] != 0, r * ulp * 0.5, torch.zeros_like(r))
+        del prev, ulp, r
+    return out
