@@ -8,41 +8,81 @@ namespace mdls {
 // A7: inverse of upper-triangular nb x nb tiles, one warp per inverse column
 // ("the k-th thread solves U v = e_k"; here the k-th WARP, its lanes
 // sharing the rows of the column-oriented back substitution).  Output is the
-// transposed inverse: Vt(c, tile*nb + r) = (U_tile^-1)(r, c).  diag_scale scales
-// the diagonal on read (0.5 builds the WY factor T from S = Y^T Y).  With
-// `dbeta` (leading limbs of the panel's beta), reflectors with beta = 0 (P = I,
-// GVL's sigma = 0 case) are decoupled: their row and column of U are treated as
-// zero off the diagonal and their column of the result is zero, which gives the
-// compact-WY factor of the remaining reflectors.
+// transposed inverse: Vt(c, tile*nb + r) = (U_tile^-1)(r, c).
+//
+// With a scaled copy Us (nb x n workspace, the back-substitution path), the
+// diagonal is absorbed first: U = D U' with U' unit upper triangular,
+// Us(i, l) = u_il / u_ii (i < l) and Us(l, l) = 1/u_ll, so U v = e_k becomes
+// U' v = e_k / u_kk and each step of the chain is x_l = s_l (no md product on
+// the latency chain, only the pivot row's normalisation and the row updates
+// s_i -= u'_il x_l, whose U' loads are issued one step ahead).  Without it
+// (mdls_invert_tiles, no workspace) every step multiplies by 1/u_ll.
 // ============================================================================
-template <int M, int NPL>
-__global__ void __launch_bounds__(256) invert_tiles_kernel(int64_t nb, CMat U, Mat Vt, double diag_scale,
-                                                           const double* dbeta, int* info) {
+// Us(i, tile*nb + l) = u_il / u_ii for i < l, 1 / u_ll on the diagonal (one CTA per tile)
+template <int M>
+__global__ void __launch_bounds__(256) scale_tiles_kernel(int64_t nb, CMat U, Mat Us, int* info) {
   extern __shared__ double smem_inv[];  // rinv: M planes of nb
+  const int64_t base = (int64_t)blockIdx.x * nb;
+  for (int64_t r = threadIdx.x; r < nb; r += blockDim.x) {
+    const md<M> d = ld<M>(U.p, U.ps, (base + r) + (base + r) * U.ld);
+    if (!(d.v[0] != 0.0) || !isfinite(d.v[0])) atomicMin(info, (int)(base + r + 1));
+    const md<M> q = div<M>(md_from<M>(1.0), d);
+#pragma unroll
+    for (int l = 0; l < M; ++l) smem_inv[l * nb + r] = q.v[l];
+    st<M>(Us.p, Us.ps, r + (base + r) * Us.ld, q);
+  }
+  __syncthreads();
+  for (int64_t e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+    const int64_t i = e % nb, l = e / nb;  // consecutive threads walk a column: coalesced
+    if (i >= l) continue;
+    md<M> ri;
+#pragma unroll
+    for (int q = 0; q < M; ++q) ri.v[q] = smem_inv[q * nb + i];
+    st<M>(Us.p, Us.ps, i + (base + l) * Us.ld, mul<M>(ld<M>(U.p, U.ps, (base + i) + (base + l) * U.ld), ri));
+  }
+}
+
+template <int M, int NPL, bool SCALED>
+__global__ void __launch_bounds__(256) invert_tiles_kernel(int64_t nb, CMat U, CMat Us, Mat Vt, int* info) {
+  extern __shared__ double smem_inv[];  // rinv: M planes of nb (unscaled path)
   const int tile = blockIdx.x;
   const int64_t base = (int64_t)tile * nb;  // tile rows/cols offset
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
 
-  for (int64_t r = tid; r < nb; r += blockDim.x) {
-    md<M> d = ld<M>(U.p, U.ps, (base + r) + (base + r) * U.ld);
-    if (diag_scale != 1.0) d = scale_pow2<M>(d, diag_scale);
-    if (dbeta && dbeta[r] == 0.0) d = md_from<M>(1.0);
-    if (!(d.v[0] != 0.0) || !isfinite(d.v[0])) atomicMin(info, (int)(base + r + 1));
-    md<M> q = div<M>(md_from<M>(1.0), d);
+  if constexpr (!SCALED) {
+    for (int64_t r = tid; r < nb; r += blockDim.x) {
+      const md<M> d = ld<M>(U.p, U.ps, (base + r) + (base + r) * U.ld);
+      if (!(d.v[0] != 0.0) || !isfinite(d.v[0])) atomicMin(info, (int)(base + r + 1));
+      const md<M> q = div<M>(md_from<M>(1.0), d);
 #pragma unroll
-    for (int l = 0; l < M; ++l) smem_inv[l * nb + r] = q.v[l];
+      for (int l = 0; l < M; ++l) smem_inv[l * nb + r] = q.v[l];
+    }
+    __syncthreads();
   }
-  __syncthreads();
+  // element (i, l) of the tile's (scaled) strictly upper part
+  auto u_at = [&](int64_t i, int64_t l) -> md<M> {
+    if constexpr (SCALED) return ld<M>(Us.p, Us.ps, i + (base + l) * Us.ld);
+    else return ld<M>(U.p, U.ps, (base + i) + (base + l) * U.ld);
+  };
 
   for (int64_t k = (int64_t)blockIdx.y * nwarp + warp; k < nb; k += (int64_t)gridDim.y * nwarp) {
-    const bool degk = dbeta && dbeta[k] == 0.0;
-    // row accumulators s_i = e_k(i) - sum_l u_il x_l (md.cuh Acc: exact deposits, normalised only
-    // when row i becomes the pivot row l)
+    // row accumulators s_i = rhs_i - sum_l u_il x_l (md.cuh Acc: exact deposits, normalised only when
+    // row i becomes the pivot row l); rhs = e_k (unscaled) or e_k / u_kk (scaled)
     Acc<M> s[NPL];
+    md<M> rk = md_from<M>(1.0);
+    if constexpr (SCALED) rk = u_at(k, k);
 #pragma unroll
     for (int t = 0; t < NPL; ++t) {
       s[t].init();
-      if (lane + 32 * t == k) s[t].r(0) = 1.0;
+      if (lane + 32 * t == k)
+#pragma unroll
+        for (int q = 0; q < M; ++q) s[t].r(q) = rk.v[q];
+    }
+    md<M> un[NPL];  // column l of the strict upper part, loaded one step ahead
+#pragma unroll
+    for (int t = 0; t < NPL; ++t) {
+      const int64_t i = lane + 32 * t;
+      un[t] = (i < k) ? u_at(i, k) : md_zero<M>();
     }
     for (int64_t l = k; l >= 0; --l) {
       const int ol = (int)(l & 31), tl = (int)(l >> 5);
@@ -51,23 +91,27 @@ __global__ void __launch_bounds__(256) invert_tiles_kernel(int64_t nb, CMat U, M
       for (int t = 1; t < NPL; ++t)
 #pragma unroll
         for (int q = 0; q < Acc<M>::NV; ++q) sa.r(q) = (t == tl) ? s[t].r(q) : sa.r(q);
-      const md<M> sl = sa.get();
-      md<M> rinv;
+      md<M> x = sa.get();
+      if constexpr (!SCALED) {
+        md<M> rinv;
 #pragma unroll
-      for (int q = 0; q < M; ++q) rinv.v[q] = smem_inv[q * nb + l];
-      md<M> x = mul<M>(sl, rinv);
+        for (int q = 0; q < M; ++q) rinv.v[q] = smem_inv[q * nb + l];
+        x = mul<M>(x, rinv);
+      }
       x = shfl<M>(x, ol);
-      if (lane == 0) st<M>(Vt.p, Vt.ps, k + (base + l) * Vt.ld, degk ? md_zero<M>() : x);
+      if (lane == 0) st<M>(Vt.p, Vt.ps, k + (base + l) * Vt.ld, x);
       const md<M> nx = neg(x);
-      const bool degl = dbeta && dbeta[l] == 0.0;
+      md<M> uc[NPL];
+#pragma unroll
+      for (int t = 0; t < NPL; ++t) {
+        uc[t] = un[t];
+        const int64_t i = lane + 32 * t;
+        un[t] = (l >= 1 && i < l - 1) ? u_at(i, l - 1) : md_zero<M>();  // next step's column, in flight
+      }
 #pragma unroll
       for (int t = 0; t < NPL; ++t) {
         const int64_t i = lane + 32 * t;
-        if (i < l) {
-          md<M> u = (degl || (dbeta && dbeta[i] == 0.0)) ? md_zero<M>()
-                                                           : ld<M>(U.p, U.ps, (base + i) + (base + l) * U.ld);
-          s[t].add_prod(u, nx);
-        }
+        if (i < l) s[t].add_prod(uc[t], nx);
       }
     }
     // zeros below the diagonal of the inverse: Vt(k, base + r) for r > k
@@ -147,17 +191,27 @@ __global__ void __launch_bounds__(32 * G) bs_update_kernel(int64_t nb, int64_t t
   }
 }
 
+// Us (nullable): nb x (ntiles nb) workspace for the row-scaled copy (the diagonal absorbed, see A7)
 template <int M>
-void launch_invert(cudaStream_t st, int64_t ntiles, int64_t nb, CMat U, Mat Vt, double diag_scale, const double* dbeta,
-                   int* info) {
+void launch_invert(cudaStream_t st, int64_t ntiles, int64_t nb, CMat U, Mat Vt, Mat Us, int* info) {
   const int threads = 256, nwarp = threads / 32;
   const int64_t ny = cdiv(nb, nwarp);
   dim3 grid((unsigned)ntiles, (unsigned)ny);
   const size_t smem = sizeof(double) * M * nb;
-  if (nb <= 32) MDLS_LAUNCH(F_INVERT, st, invert_tiles_kernel<M, 1><<<grid, threads, smem, st>>>(nb, U, Vt, diag_scale, dbeta, info));
-  else if (nb <= 64) MDLS_LAUNCH(F_INVERT, st, invert_tiles_kernel<M, 2><<<grid, threads, smem, st>>>(nb, U, Vt, diag_scale, dbeta, info));
-  else if (nb <= 128) MDLS_LAUNCH(F_INVERT, st, invert_tiles_kernel<M, 4><<<grid, threads, smem, st>>>(nb, U, Vt, diag_scale, dbeta, info));
-  else MDLS_LAUNCH(F_INVERT, st, invert_tiles_kernel<M, 8><<<grid, threads, smem, st>>>(nb, U, Vt, diag_scale, dbeta, info));
+  if (Us.p) {
+    MDLS_LAUNCH(F_INVERT, st, scale_tiles_kernel<M><<<(unsigned)ntiles, threads, smem, st>>>(nb, U, Us, info));
+    const CMat C = cm(Us);
+    if (nb <= 32) MDLS_LAUNCH(F_INVERT, st, invert_tiles_kernel<M, 1, true><<<grid, threads, 0, st>>>(nb, U, C, Vt, info));
+    else if (nb <= 64) MDLS_LAUNCH(F_INVERT, st, invert_tiles_kernel<M, 2, true><<<grid, threads, 0, st>>>(nb, U, C, Vt, info));
+    else if (nb <= 128) MDLS_LAUNCH(F_INVERT, st, invert_tiles_kernel<M, 4, true><<<grid, threads, 0, st>>>(nb, U, C, Vt, info));
+    else MDLS_LAUNCH(F_INVERT, st, invert_tiles_kernel<M, 8, true><<<grid, threads, 0, st>>>(nb, U, C, Vt, info));
+    return;
+  }
+  const CMat C{nullptr, 0, 0};
+  if (nb <= 32) MDLS_LAUNCH(F_INVERT, st, invert_tiles_kernel<M, 1, false><<<grid, threads, smem, st>>>(nb, U, C, Vt, info));
+  else if (nb <= 64) MDLS_LAUNCH(F_INVERT, st, invert_tiles_kernel<M, 2, false><<<grid, threads, smem, st>>>(nb, U, C, Vt, info));
+  else if (nb <= 128) MDLS_LAUNCH(F_INVERT, st, invert_tiles_kernel<M, 4, false><<<grid, threads, smem, st>>>(nb, U, C, Vt, info));
+  else MDLS_LAUNCH(F_INVERT, st, invert_tiles_kernel<M, 8, false><<<grid, threads, smem, st>>>(nb, U, C, Vt, info));
 }
 
 template <int M>
@@ -167,7 +221,8 @@ void launch_bs_mulinv(cudaStream_t st, int64_t nb, int64_t tile, CMat Vt, const 
 }
 
 // rows [row0, row1): CTA = 32 rows x GC column groups (1024 / 512 threads), so
-// even the short late steps spread over many SMs
+// even the short late steps spread over many SMs; `critical` (one tile of rows on the
+// back substitution's chain): twice the column groups, half the sequential products
 template <int M>
 void launch_bs_update(cudaStream_t st, int64_t nb, int64_t tile, int64_t row0, int64_t row1, CMat U, const double* x,
                       int64_t psx, double* b, int64_t psb) {
@@ -178,7 +233,7 @@ void launch_bs_update(cudaStream_t st, int64_t nb, int64_t tile, int64_t row0, i
 }
 
 #define MDLS_INSTANTIATE_BS(MM)                                                                                \
-  template void launch_invert<MM>(cudaStream_t, int64_t, int64_t, CMat, Mat, double, const double*, int*);                    \
+  template void launch_invert<MM>(cudaStream_t, int64_t, int64_t, CMat, Mat, Mat, int*);                                     \
   template void launch_bs_mulinv<MM>(cudaStream_t, int64_t, int64_t, CMat, const double*, int64_t, double*,    \
                                      int64_t);                                                                 \
   template void launch_bs_update<MM>(cudaStream_t, int64_t, int64_t, int64_t, int64_t, CMat, const double*,  \

@@ -45,8 +45,7 @@ cudaError_t launch_leaf_chain(cudaStream_t st, int64_t Mrows, int64_t js, int B,
                               int64_t bps, Mat T, int* info, Mat Tp, int64_t jsp);
 
 template <int M>
-void launch_invert(cudaStream_t st, int64_t ntiles, int64_t nb, CMat U, Mat Vt, double diag_scale, const double* dbeta,
-                   int* info);
+void launch_invert(cudaStream_t st, int64_t ntiles, int64_t nb, CMat U, Mat Vt, Mat Us, int* info);
 
 template <int M>
 void launch_bs_mulinv(cudaStream_t st, int64_t nb, int64_t tile, CMat Vt, const double* b, int64_t psb, double* x,

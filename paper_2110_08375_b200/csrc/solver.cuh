@@ -24,7 +24,7 @@ namespace mdls {
 // workspace plan (bytes, 256-aligned segments)
 // ---------------------------------------------------------------------------
 struct Plan {
-  size_t af = 0, q = 0, y = 0, w = 0, beta = 0, s = 0, t = 0, x = 0, part = 0, v0 = 0, v1 = 0, v2 = 0, vt = 0,
+  size_t af = 0, q = 0, y = 0, w = 0, beta = 0, s = 0, t = 0, x = 0, part = 0, v0 = 0, v1 = 0, v2 = 0, vt = 0, us = 0,
          info = 0, total = 0;
 };
 
@@ -64,7 +64,10 @@ Plan make_plan(int op, int64_t Mr, int64_t K, int64_t nb) {
   p.v0 = take(md * mx);
   p.v1 = take(md * mx);
   p.v2 = take(md * mx);
-  if (op == MDLS_OP_BACKSUB || op == MDLS_OP_LSTSQ || op == MDLS_OP_LSTSQ_NOQ) p.vt = take(md * nb * K);
+  if (op == MDLS_OP_BACKSUB || op == MDLS_OP_LSTSQ || op == MDLS_OP_LSTSQ_NOQ) {
+    p.vt = take(md * nb * K);
+    p.us = take(md * nb * K);  // row-scaled diagonal tiles (tile inversion)
+  }
   p.info = take(4 * sizeof(int));
   p.total = off;
   return p;
@@ -461,49 +464,52 @@ void apply_qt_panels(cudaStream_t st, int64_t Mr, int64_t K, int64_t nb, CMat Y,
 }
 
 // Algorithm 1: U x = y (leading n x n of U), N = n/nb tiles.
-// Tile inverses are computed in chunks of 16 tiles, top first, on a side stream
-// so that the chain can start as soon as the last tiles are inverted; the chain
-// i = N..1 runs on `st`: x_i = U_i^-1 b_i, then b_j -= A_ji x_i for all j < i
-// in one launch (the paper's "simultaneously update").
+// The tile inverses are computed in chunks of tiles, bottom first, on a
+// low-priority side stream; the chain i = N..1 (x_i = U_i^-1 b_i, then
+// b_j -= A_ji x_i for all j < i in one launch: the paper's "simultaneously
+// update") runs on a high-priority side stream and starts as soon
+// as the bottom chunk is inverted.
 template <int M>
 void backsub(cudaStream_t st, int64_t n, int64_t nb, CMat U, const double* y, int64_t psy, double* x, int64_t psx,
-             Mat Vt, double* bwork, int* info_slot) {
+             Mat Vt, Mat Us, double* bwork, int* info_slot) {
   const int64_t N = n / nb;
-  cudaStream_t sinv = side_stream(1);
+  cudaStream_t sinv = side_stream(3), sch = side_stream(0);
   auto fork = [](cudaStream_t from, cudaStream_t to) {
     cudaEvent_t ev = pool_event();
     cudaEventRecord(ev, from);
     cudaStreamWaitEvent(to, ev, 0);
   };
   fork(st, sinv);
+  fork(st, sch);
   set_stage(MDLS_ST_INVERT);
   static const int64_t chunk_env = [] {
     const char* v = getenv("MDLS_INV_CHUNK");
-    return (int64_t)(v ? atoi(v) : 0);  // 0: all tiles in one launch (measured 5.41 vs 5.50 ms at n = 17920)
+    return (int64_t)(v ? atoi(v) : 16);  // tiles per inversion launch, bottom first (0: all in one launch)
   }();
   const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(N, chunk_env > 0 ? chunk_env : N));
   std::vector<cudaEvent_t> inv_ready((size_t)N, nullptr);
   for (int64_t hi = N; hi > 0; hi -= chunk) {
     const int64_t lo = std::max<int64_t>(0, hi - chunk);
-    launch_invert<M>(sinv, hi - lo, nb, sub(U, lo * nb, lo * nb), sub(Vt, 0, lo * nb), 1.0, nullptr, info_slot);
+    launch_invert<M>(sinv, hi - lo, nb, sub(U, lo * nb, lo * nb), sub(Vt, 0, lo * nb), sub(Us, 0, lo * nb), info_slot);
     cudaEvent_t ev = pool_event();
     cudaEventRecord(ev, sinv);
     for (int64_t t = lo; t < hi; ++t) inv_ready[(size_t)t] = ev;
   }
   // bwork = y (n entries)
-  MDLS_LAUNCH(F_MISC, st, copy_kernel<M><<<grid_for(n, 256), 256, 0, st>>>(n, 1, CMat{y, n, psy}, Mat{bwork, n, n}, 0));
+  MDLS_LAUNCH(F_MISC, sch, copy_kernel<M><<<grid_for(n, 256), 256, 0, sch>>>(n, 1, CMat{y, n, psy}, Mat{bwork, n, n}, 0));
   cudaEvent_t waited = nullptr;
   for (int64_t i = N - 1; i >= 0; --i) {
     if (inv_ready[(size_t)i] != waited) {
-      cudaStreamWaitEvent(st, inv_ready[(size_t)i], 0);
+      cudaStreamWaitEvent(sch, inv_ready[(size_t)i], 0);
       waited = inv_ready[(size_t)i];
     }
     set_stage(MDLS_ST_MULINV);
-    launch_bs_mulinv<M>(st, nb, i, cm(Vt), bwork, n, x, psx);
+    launch_bs_mulinv<M>(sch, nb, i, cm(Vt), bwork, n, x, psx);
     set_stage(MDLS_ST_BSUPDATE);
-    if (i >= 1) launch_bs_update<M>(st, nb, i, 0, i * nb, U, x, psx, bwork, n);
+    if (i >= 1) launch_bs_update<M>(sch, nb, i, 0, i * nb, U, x, psx, bwork, n);
   }
   fork(sinv, st);
+  fork(sch, st);
 }
 
 }  // namespace mdls
