@@ -37,6 +37,7 @@ WORKLOADS = {
     "cfg3qd": ("qd", 1024, 1024, 128),
     "cfg3od": ("od", 1024, 1024, 128),
     "cfg5b": ("dd", 1024, 1024, 128),  # + BATCH_5B independent problems sharded over the ranks
+    "cfg5a": ("od", 8192, 8192, 128),  # block-column sharded QR + lstsq (sharded.py), --size overrides M = K
 }
 BATCH_5B = 256
 BATCH_CHUNK = 32  # problems per captured CUDA graph (one mdls_lstsq_batched call each)
@@ -67,6 +68,7 @@ def parse():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--groups", type=int, default=8, help="stream groups of the batched solves (cfg5b)")
     ap.add_argument("--batch", type=int, default=BATCH_5B, help="problems of the cfg5b batch (all ranks)")
+    ap.add_argument("--size", type=int, default=0, help="cfg5a: M = K (default 8192)")
     return ap.parse_args()
 
 
@@ -216,6 +218,8 @@ def run_ours(args, ws, rank, local):
     prec, M, K, nb = WORKLOADS[args.workload]
     if args.workload == "cfg5b":
         return run_batch_workload(args, ws, rank, dev, barrier, max_over_ranks)
+    if args.workload == "cfg5a":
+        return run_sharded_workload(args, ws, rank, dev, barrier, max_over_ranks)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
 
     def measure(prec, M, K, nb, steps, warmup, seed, with_e2e, with_trace, sampler=None):
@@ -440,6 +444,71 @@ def run_batch_workload(args, ws, rank, dev, barrier, max_over_ranks):
         "e2e": {"value": round(flops / (r["e2e_ms"] * 1e-3) / 1e9, 2), "unit": "GFLOP/s",
                 "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"], "ms_per_step": round(r["e2e_ms"], 3)},
         "gpu_launches": int(r["launches_per_step"] * args.steps),
+    }
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+
+
+def run_sharded_workload(args, ws, rank, dev, barrier, max_over_ranks):
+    """--workload cfg5a: BASELINE config 5a, the block-column sharded QR + least squares (sharded.py) of an od
+    M x M matrix (default 8192) over the ranks: panel k on rank k mod N, W_k / Y_k NCCL-broadcast from the owner
+    (row-trimmed), look-ahead panel on a high-priority stream; fixed total work (strong scaling)."""
+    import torch
+
+    import paper_2110_08375_b200 as mdls
+    from paper_2110_08375_b200 import inputs, sharded
+
+    prec, M, K, nb = WORKLOADS["cfg5a"]
+    if args.size:
+        M = K = args.size
+    st = sharded.plan(prec, M, K, nb, ws)
+    A = inputs.random_matrix_torch(M, K, prec, seed=5, device=dev)  # every rank generates the same A ...
+    b = inputs.random_vector_torch(M, prec, seed=5, device=dev)
+    A_src = {rank: A[:, sharded.local_columns(st, rank), :].contiguous()}  # ... and keeps its own panels
+    del A
+    torch.cuda.empty_cache()
+    comm = sharded.Comm() if ws > 1 else None
+    ops = sharded.GpuOps()
+    new = lambda shape: torch.zeros(shape, dtype=torch.float64, device=dev)  # noqa: E731
+
+    def step():
+        A_loc = {r: t.clone() for r, t in A_src.items()}
+        return sharded.sharded_lstsq(prec, A_loc, b, M, K, nb, ws, ops, comm, new, sharded.Streams(dev))
+
+    for _ in range(max(1, args.warmup)):
+        x, F, y, info = step()
+    torch.cuda.synchronize()
+    assert int(info.item()) == 0
+    sampler = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier()
+    torch.cuda.synchronize()
+    n0 = mdls.launch_count()
+    with sampler:
+        for i in range(args.steps):
+            ev[i][0].record()
+            x, F, y, info = step()
+            ev[i][1].record()
+        torch.cuda.synchronize()
+    launches = mdls.launch_count() - n0
+    barrier()
+    ms = max_over_ranks(sum(a.elapsed_time(bb) for a, bb in ev) / args.steps)
+    flops = ledger_flops(prec, M, K, nb)["total_flops"]
+    value = flops / (ms * 1e-3) / 1e9
+    res = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{prec} least squares {M}x{K}, tile {nb}, block-column sharded over {ws} GPU(s) "
+                               "(sharded.py: panel k on rank k mod N, W/Y NCCL broadcast, look-ahead)",
+                   "precision": prec, "M": M, "K": K, "nb": nb, "parallelism": f"colshard{ws}",
+                   "l2": "operands exceed L2", "graph": False, "flops_per_solve": flops},
+        "fp64_peak_frac": round(value / ws / (FP64_PEAK_TFLOPS * 1e3), 4),
+        "clocks": sampler.summary(), "gpu_launches": int(launches),
     }
     if ws > 1:
         import torch.distributed as dist

@@ -217,11 +217,14 @@ int mdls_trace_collect(double *stage_ms, double *family_ms, int64_t *family_laun
    * qr_panel: factor panel k, i.e. the columns [k*nb, (k+1)*nb) of A passed as the M x nb operand Ak (rows        \
    * 0..M-1, all earlier panels already applied), M >= (k+1)*nb; on return Ak holds R and v like mdls_qr, and     \
    * Wk, Yk (M x nb, rows < k*nb zero) hold the panel's W and explicit Y (unit diagonal): P_WY = I + Wk Yk^T.      \
-   * dev_info as for mdls_qr (global 1-based row). */                                                              \
+   * dev_info as for mdls_qr (global 1-based row).  Wk and Yk are only accessed on rows k*nb..M-1, so a caller    \
+   * may keep just those rows (the sharded driver broadcasts them): pass the buffer pointer minus k*nb, ld >=       \
+   * M - k*nb (the same holds for qr_update's Wk, Yk). */                                                            \
   int mdls_qr_panel_##P(int64_t M, int64_t nb, int64_t k, double *Ak, int64_t lda, int64_t psa, double *Wk,        \
                         int64_t ldw, int64_t psw, double *Yk, int64_t ldy, int64_t psy, void *work,                 \
                         size_t work_bytes, int *dev_info, void *stream);                                           \
-  /* qr_update: C += Yk (Wk^T C) for the columns [c0, c1) of A, rows k*nb..M-1 ("YWT * C", "R + YWTC").            \
+  /* qr_update: C += Yk (Wk^T C) for the columns [c0, c1) of A (c1 <= M), rows k*nb..M-1 ("YWT * C", "R + YWTC"); \
+   * work: mdls_workspace_<p>(MDLS_OP_QR, M, nb, nb) bytes.                                                         \
    * With Wk and Yk exchanged it computes C += Wk (Yk^T C): the backward Q-formation step on a column block. */   \
   int mdls_qr_update_##P(int64_t M, int64_t nb, int64_t k, const double *Wk, int64_t ldw, int64_t psw,             \
                          const double *Yk, int64_t ldy, int64_t psy, double *A, int64_t lda, int64_t psa,          \

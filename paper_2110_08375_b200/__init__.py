@@ -402,32 +402,39 @@ def _view(t, col0: int, ncols: int):
     return ctypes.c_void_p(t.data_ptr() + 8 * col0 * ld), ld, t.shape[1] * ld
 
 
+def _trimmed(t, row0: int):
+    """(ptr, ld, ps) of an (m, cols, ld) tensor holding only rows row0.. of an operand indexed by global row:
+    the pointer is moved back by row0 rows (rows < row0 are never accessed, include/mdls.h)."""
+    return ctypes.c_void_p(t.data_ptr() - 8 * row0), t.shape[2], t.shape[1] * t.shape[2]
+
+
 def qr_panel(prec: str, A, col0: int, k: int, nb: int, W, Y, work=None):
-    """Factor panel k stored in columns [col0, col0+nb) of A (rows global); W and Y
-    (m, nb, M) receive the panel's P_WY = I + W Y^T.  Returns the device info tensor."""
-    torch = _torch()
+    """Factor panel k stored in columns [col0, col0+nb) of A (rows global); W and Y receive the panel's
+    P_WY = I + W Y^T, either as full (m, nb, M) tensors or row-trimmed (m, nb, M - k nb) ones (rows k nb..M-1).
+    Returns the device info tensor."""
     M = A.shape[2]
     if work is None:
         work, nbytes = _work(prec, _lib.OP_QR, M, nb, nb, A.device)
     else:
         nbytes = work.numel()
     info = _info(A.device)
-    rc = _lib.fn("mdls_qr_panel_", prec)(M, nb, k, *_view(A, col0, nb), *_mat(W), *_mat(Y), _ptr(work), nbytes,
-                                         _ptr(info), _stream())
+    r0 = M - W.shape[2]
+    rc = _lib.fn("mdls_qr_panel_", prec)(M, nb, k, *_view(A, col0, nb), *_trimmed(W, r0), *_trimmed(Y, r0),
+                                         _ptr(work), nbytes, _ptr(info), _stream())
     _lib.check(rc, "qr_panel")
     return info
 
 
 def qr_update(prec: str, Wk, Yk, A, k: int, nb: int, c0: int, c1: int, work=None):
-    """C += Yk (Wk^T C) on columns [c0, c1) of A (rows k*nb..M-1)."""
+    """C += Yk (Wk^T C) on columns [c0, c1) of A (rows k*nb..M-1); Wk, Yk full or row-trimmed as in qr_panel."""
     M = A.shape[2]
     if c1 <= c0:
         return
     if work is None:
-        Kw = -(-max(c1, nb) // nb) * nb
-        work, nbytes = _work(prec, _lib.OP_QR, max(M, Kw), Kw, nb, A.device)
+        work, nbytes = _work(prec, _lib.OP_QR, M, nb, nb, A.device)
     else:
         nbytes = work.numel()
-    rc = _lib.fn("mdls_qr_update_", prec)(M, nb, k, *_mat(Wk), *_mat(Yk), *_mat(A), c0, c1, _ptr(work), nbytes,
-                                          _stream())
+    r0 = M - Wk.shape[2]
+    rc = _lib.fn("mdls_qr_update_", prec)(M, nb, k, *_trimmed(Wk, r0), *_trimmed(Yk, r0), *_mat(A), c0, c1,
+                                          _ptr(work), nbytes, _stream())
     _lib.check(rc, "qr_update")

@@ -451,8 +451,9 @@ int MDLS_FN(mdls_qr_panel_)(int64_t Mr, int64_t nb, int64_t k, double* Ak, int64
   if (nb < 1 || nb > 256) return -2;
   if (k < 0 || (k + 1) * nb > Mr) return -3;
   if (!mat_ok(Ak, Mr, nb, lda, psa)) return -4;
-  if (!mat_ok(Wk, Mr, nb, ldw, psw)) return -7;
-  if (!mat_ok(Yk, Mr, nb, ldy, psy)) return -10;
+  // Wk, Yk are only touched on rows k*nb..M-1: a row-trimmed buffer may be passed (ld >= M - k*nb)
+  if (!mat_ok(Wk, Mr - k * nb, nb, ldw, psw)) return -7;
+  if (!mat_ok(Yk, Mr - k * nb, nb, ldy, psy)) return -10;
   const Plan p = make_plan<M>(MDLS_OP_QR, Mr, nb, nb);
   if (!work || work_bytes < p.total) return -14;
   cudaStream_t st = S(stream);
@@ -463,8 +464,8 @@ int MDLS_FN(mdls_qr_panel_)(int64_t Mr, int64_t nb, int64_t k, double* Ak, int64
   QrBufs<M> b = qr_bufs(work, p, Mr, nb, nb, nullptr, 0, 0);
   MDLS_LAUNCH(F_MISC, st, info_init_kernel<<<1, 1, 0, st>>>(b.info_slot));
   for (int l = 0; l < M; ++l) {
-    cudaMemset2DAsync(Wk + l * psw, sizeof(double) * ldw, 0, sizeof(double) * Mr, nb, st);
-    cudaMemset2DAsync(Yk + l * psy, sizeof(double) * ldy, 0, sizeof(double) * Mr, nb, st);
+    cudaMemset2DAsync(Wk + l * psw + j0, sizeof(double) * ldw, 0, sizeof(double) * (Mr - j0), nb, st);
+    cudaMemset2DAsync(Yk + l * psy + j0, sizeof(double) * ldy, 0, sizeof(double) * (Mr - j0), nb, st);
   }
   // beta: per panel, stored in the workspace (indexed by global column)
   const Lane L = b.lane(0, st);
@@ -479,15 +480,17 @@ int MDLS_FN(mdls_qr_update_)(int64_t Mr, int64_t nb, int64_t k, const double* Wk
   if (Mr < 1) return -1;
   if (nb < 1 || nb > 256) return -2;
   if (k < 0 || (k + 1) * nb > Mr) return -3;
-  if (!mat_ok(Wk, Mr, nb, ldw, psw)) return -4;
-  if (!mat_ok(Yk, Mr, nb, ldy, psy)) return -7;
+  if (!mat_ok(Wk, Mr - k * nb, nb, ldw, psw)) return -4;  // rows k*nb..M-1 only (see mdls_qr_panel)
+  if (!mat_ok(Yk, Mr - k * nb, nb, ldy, psy)) return -7;
   if (c0 < 0 || c1 < c0) return -13;
   if (!mat_ok(A, Mr, c1, lda, psa)) return -10;
-  const Plan p = make_plan<M>(MDLS_OP_QR, std::max<int64_t>(Mr, c1), std::max<int64_t>(c1, nb), nb);
+  if (c1 > Mr) return -14;
+  // scratch: one GEMM lane (X = W^T C, nb x (c1 - c0) <= nb x M, and split-K partials): the plan of a one-panel QR
+  const Plan p = make_plan<M>(MDLS_OP_QR, Mr, nb, nb);
   if (!work || work_bytes < p.total) return -16;
   cudaStream_t st = S(stream);
   set_stage(MDLS_NSTAGES);
-  QrBufs<M> b = qr_bufs(work, p, std::max<int64_t>(Mr, c1), std::max<int64_t>(c1, nb), nb, nullptr, 0, 0);
+  QrBufs<M> b = qr_bufs(work, p, Mr, nb, nb, nullptr, 0, 0);
   const int64_t j0 = k * nb;
   qr_apply_panel<M>(b.lane(0, st), Mr, nb, k, CMat{Yk + j0, ldy, psy}, CMat{Wk + j0, ldw, psw}, Mat{A, lda, psa}, c0,
                     c1);

@@ -52,18 +52,20 @@ class PlainOps(sharded.Ops):
             v = Ym[:, l]
             Wm[:, l] = -betas[l] * (v + Wm[:, :l] @ (Ym[:, :l].T @ v))
         A[0, col0:col0 + nb, :] = torch.from_numpy(P.T.copy())
+        r0 = M - W.shape[2]  # row-trimmed panel buffers hold rows r0..M-1
         W.zero_()
         Y.zero_()
-        W[0] = torch.from_numpy(Wm.T.copy())
-        Y[0] = torch.from_numpy(Ym.T.copy())
+        W[0] = torch.from_numpy(Wm.T[:, r0:].copy())
+        Y[0] = torch.from_numpy(Ym.T[:, r0:].copy())
 
     def update(self, prec, Wk, Yk, A, k, nb, c0, c1):
         if c1 <= c0:
             return
         j0 = k * nb
+        r0 = A.shape[2] - Wk.shape[2]
         C = A[0, c0:c1, j0:].numpy().T  # (rows, cols)
-        Wm = Wk[0, :, j0:].numpy().T
-        Ym = Yk[0, :, j0:].numpy().T
+        Wm = Wk[0, :, j0 - r0:].numpy().T
+        Ym = Yk[0, :, j0 - r0:].numpy().T
         C2 = C + Ym @ (Wm.T @ C)
         A[0, c0:c1, j0:] = torch.from_numpy(C2.T.copy())
 
@@ -90,7 +92,7 @@ def run_sharded(A, nb, P, local_ranks, comm):
     st = sharded.plan("dd", M, K, nb, P)
     A_loc = {r: A[:, sharded.local_columns(st, r), :].clone() for r in local_ranks}
     new = lambda shape: torch.zeros(shape, dtype=torch.float64)
-    W, Y = sharded.sharded_qr(st, A_loc, PlainOps(), comm, new)
+    W, Y, _ = sharded.sharded_qr(st, A_loc, PlainOps(), comm, new)
     Q = sharded.sharded_form_q(st, W, Y, PlainOps(), new, local_ranks)
     return st, A_loc, Q
 
