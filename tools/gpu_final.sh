@@ -1,8 +1,9 @@
-# round measurement: GPU tests, default bench (with cpu baseline), launch list, ncu full of the leaf kernel
-timeout 1200 python -m pytest tests -m gpu -q 2>&1 | tail -3 > gpurun_out/final_tests.txt
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/final_gpu.txt
-timeout 900 python bench.py > gpurun_out/final_bench.json 2> gpurun_out/final_bench.err
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/final_launches.csv python tools/prof_step.py dd 1024 128 1 > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:leaf_reg_kernel -s 20 -c 1 -o gpurun_out/final_leaf python tools/prof_step.py dd 1024 128 1 > /dev/null 2>&1
-timeout 300 python bench.py --impl reference --steps 1 --warmup 0 > gpurun_out/final_ref.json 2> gpurun_out/final_ref.err
-cat gpurun_out/final_tests.txt; head -c 600 gpurun_out/final_bench.json; echo; cat gpurun_out/final_ref.json | head -c 400
+set -x
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+timeout 1200 python bench.py > gpurun_out/bench_final.json 2> gpurun_out/bench_final.err; tail -c 6000 gpurun_out/bench_final.json; tail -3 gpurun_out/bench_final.err
+timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2>&1; tail -c 800 gpurun_out/bench_ref.json
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemm_kernel -c 1 -o gpurun_out/gemm_dd_final -f python tools/prof_gemm.py dd 1024 128 1 > /dev/null 2>&1
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:leaf_reg_kernel -s 20 -c 1 -o gpurun_out/leaf_dd_final -f python tools/time_variants.py dd 1024 128 > /dev/null 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_dd_final.csv python bench.py --steps 1 --warmup 1 --no-extra --no-cpu --no-graph > /dev/null 2>&1
+ls -la gpurun_out/*.ncu-rep gpurun_out/launches_dd_final.csv
