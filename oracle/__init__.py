@@ -69,6 +69,7 @@ def _load(counting: bool = False) -> ctypes.CDLL:
     lib.oracle_qt_b_explicit.argtypes = [ctypes.c_int, _I64, _D, _I64, _D, _D, ctypes.c_int]
     lib.oracle_backsub.argtypes = [ctypes.c_int, _I64, _D, _I64, _I64, _D, _I64, _D]
     lib.oracle_lstsq.argtypes = [ctypes.c_int, _I64, _I64, _D, _I64, _D, _D, _D, _D, ctypes.c_int]
+    lib.oracle_zlstsq.argtypes = [ctypes.c_int, _I64, _I64, _D, _D, _I64, _D, _D, _D, _D, _D, _D]
     lib.oracle_inv_orth.argtypes = [ctypes.c_int, _I64, _D, _I64, ctypes.POINTER(_I64), _I64, ctypes.c_int]
     lib.oracle_inv_orth.restype = ctypes.c_double
     lib.oracle_inv_recon.argtypes = [ctypes.c_int, _I64, _I64, _D, _I64, _D, _I64, _D, _I64,
@@ -235,6 +236,24 @@ def backsub(prec, R: np.ndarray, y: np.ndarray, n: int | None = None) -> tuple[n
     x = np.zeros((m, n))
     info = _load().oracle_backsub(m, n, _p(R), ld, cols, _p(y), y.shape[1], _p(x))
     return x, int(info)
+
+
+def zlstsq(prec, Are: np.ndarray, Aim: np.ndarray, bre: np.ndarray, bim: np.ndarray):
+    """Complex least squares (unblocked complex Householder QR with Hermitian reflectors, Q^H b, complex back
+    substitution; mdls_oracle.c oracle_zlstsq).  Re/im parts as separate (m, K, M) / (m, M) arrays.
+    Returns (xre, xim, Rre, Rim, info); R_jj = -phase(x_1) ||x|| (complex)."""
+    m = _m_of(prec)
+    Are = np.ascontiguousarray(Are, dtype=np.float64)
+    Aim = np.ascontiguousarray(Aim, dtype=np.float64)
+    _, K, M = Are.shape
+    bre = np.ascontiguousarray(bre, dtype=np.float64)
+    bim = np.ascontiguousarray(bim, dtype=np.float64)
+    xre, xim = np.zeros((m, K)), np.zeros((m, K))
+    Rre, Rim = np.zeros_like(Are), np.zeros_like(Aim)
+    info = _load().oracle_zlstsq(m, M, K, _p(Are), _p(Aim), M, _p(bre), _p(bim), _p(xre), _p(xim), _p(Rre), _p(Rim))
+    if info < 0:
+        raise ValueError(f"oracle_zlstsq rc={info}")
+    return xre, xim, Rre, Rim, info
 
 
 def lstsq(prec, A: np.ndarray, b: np.ndarray, nthreads: int = 0):

@@ -1221,6 +1221,208 @@ int oracle_blocked(int op, int m, int64_t M, int64_t K, int64_t nb, const double
   return info;
 }
 
+/* ------------------------------------------------------------------------- */
+/* complex least squares (row f2; "real and complex matrices",      */
+/* P:384-385 real and imaginary parts kept separately, P:515-516 the          */
+/* transpose replaced by the Hermitian transpose).  A complex md number is    */
+/* the pair (re, im) of md numbers; arithmetic is the schoolbook definition:  */
+/*   (a + bi)(c + di) = (ac - bd) + (ad + bc) i,   conj(a + bi) = a - bi,      */
+/*   |z|^2 = a^2 + b^2,  1/z = conj(z) / |z|^2.                                */
+/* Unblocked complex Householder QR: for column j, x = A(j:M, j),             */
+/*   mu = ||x||_2 = sqrt(|x_1|^2 + sigma), sigma = sum_{i>1} |x_i|^2,         */
+/*   phase = x_1 / |x_1| (1 when x_1 = 0), alpha = -phase mu,                 */
+/*   v = x - alpha e_1 (v_1 = phase (|x_1| + mu), no cancellation),           */
+/*   v <- v / v_1, beta = 2 / (v^H v),  H = I - beta v v^H (Hermitian,        */
+/*   unitary), H x = alpha e_1, R_jj = alpha; sigma = 0 and Im x_1 = 0:        */
+/*   H = I, R_jj = x_1.  Columns c > j: w = v^H a_c, a_c -= beta v w.         */
+/* Q^H b by the reflectors in order, then complex back substitution.          */
+/* Storage: re and im parts in separate limb-planar arrays.       */
+/* ------------------------------------------------------------------------- */
+static void z_mul(int m, const double *ar, const double *ai, const double *br, const double *bi, double *cr,
+                  double *ci) {
+  double t1[MAXM], t2[MAXM], t3[MAXM], t4[MAXM];
+  md_mul(m, ar, br, t1);
+  md_mul(m, ai, bi, t2);
+  md_mul(m, ar, bi, t3);
+  md_mul(m, ai, br, t4);
+  md_sub(m, t1, t2, cr);
+  md_add(m, t3, t4, ci);
+}
+/* conj(a) b */
+static void z_cmul(int m, const double *ar, const double *ai, const double *br, const double *bi, double *cr,
+                   double *ci) {
+  double nai[MAXM];
+  md_neg(m, ai, nai);
+  z_mul(m, ar, nai, br, bi, cr, ci);
+}
+static void z_abs2(int m, const double *ar, const double *ai, double *c) {
+  double t1[MAXM], t2[MAXM];
+  md_mul(m, ar, ar, t1);
+  md_mul(m, ai, ai, t2);
+  md_add(m, t1, t2, c);
+}
+/* a / b = a conj(b) / |b|^2 */
+static void z_div(int m, const double *ar, const double *ai, const double *br, const double *bi, double *cr,
+                  double *ci) {
+  double nbi[MAXM], tr[MAXM], ti[MAXM], d[MAXM];
+  md_neg(m, bi, nbi);
+  z_mul(m, ar, ai, br, nbi, tr, ti);
+  z_abs2(m, br, bi, d);
+  md_div(m, tr, d, cr);
+  md_div(m, ti, d, ci);
+}
+
+int oracle_zlstsq(int m, int64_t M, int64_t K, const double *Are, const double *Aim, int64_t lda, const double *bre,
+                  const double *bim, double *xre, double *xim, double *Rre, double *Rim) {
+  if (m != 2 && m != 4 && m != 8) return -2;
+  if (M < K || K < 1) return -3;
+  /* working copies, element-major (m limbs contiguous): F(i, j) at ((j * M + i) * m) */
+  double *Fr = malloc(sizeof(double) * m * M * K), *Fi = malloc(sizeof(double) * m * M * K);
+  double *yr = malloc(sizeof(double) * m * M), *yi = malloc(sizeof(double) * m * M);
+  double *vr = malloc(sizeof(double) * m * M), *vi = malloc(sizeof(double) * m * M);
+  double *xr_ = malloc(sizeof(double) * m * K), *xi_ = malloc(sizeof(double) * m * K);
+  for (int64_t j = 0; j < K; ++j)
+    for (int64_t i = 0; i < M; ++i)
+      for (int k = 0; k < m; ++k) {
+        Fr[(j * M + i) * m + k] = Are[(int64_t)k * lda * K + j * lda + i];
+        Fi[(j * M + i) * m + k] = Aim[(int64_t)k * lda * K + j * lda + i];
+      }
+  for (int64_t i = 0; i < M; ++i)
+    for (int k = 0; k < m; ++k) {
+      yr[i * m + k] = bre[(int64_t)k * M + i];
+      yi[i * m + k] = bim[(int64_t)k * M + i];
+    }
+#define FR(i, j) (&Fr[((j) * M + (i)) * m])
+#define FI(i, j) (&Fi[((j) * M + (i)) * m])
+  int info = 0;
+  for (int64_t j = 0; j < K; ++j) {
+    const int64_t n = M - j;
+    double sigma[MAXM], t[MAXM], a1[MAXM], mu[MAXM], beta[MAXM];
+    md_zero(m, sigma);
+    for (int64_t i = 1; i < n; ++i) { /* sigma = sum_{i>1} |x_i|^2, ascending */
+      z_abs2(m, FR(j + i, j), FI(j + i, j), t);
+      md_add(m, sigma, t, sigma);
+    }
+    const int identity = md_lead(sigma) == 0.0 && md_lead(FI(j, j)) == 0.0;
+    if (identity) {
+      md_zero(m, beta);
+    } else {
+      double x1r[MAXM], x1i[MAXM], pr[MAXM], pi[MAXM], ar[MAXM], ai[MAXM], v1r[MAXM], v1i[MAXM];
+      md_copy(m, FR(j, j), x1r);
+      md_copy(m, FI(j, j), x1i);
+      z_abs2(m, x1r, x1i, t);
+      md_sqrt(m, t, a1); /* |x_1| */
+      md_add(m, t, sigma, t);
+      md_sqrt(m, t, mu); /* mu = ||x|| */
+      if (md_lead(a1) == 0.0) {
+        md_set_d(m, 1.0, pr);
+        md_zero(m, pi);
+      } else {
+        md_div(m, x1r, a1, pr);
+        md_div(m, x1i, a1, pi);
+      }
+      md_mul(m, pr, mu, ar); /* alpha = -phase mu */
+      md_neg(m, ar, ar);
+      md_mul(m, pi, mu, ai);
+      md_neg(m, ai, ai);
+      md_add(m, a1, mu, t); /* v_1 = phase (|x_1| + mu) */
+      md_mul(m, pr, t, v1r);
+      md_mul(m, pi, t, v1i);
+      /* v = x / v_1, v_1 = 1 */
+      md_set_d(m, 1.0, &vr[0]);
+      md_zero(m, &vi[0]);
+      for (int64_t i = 1; i < n; ++i) z_div(m, FR(j + i, j), FI(j + i, j), v1r, v1i, &vr[i * m], &vi[i * m]);
+      /* beta = 2 / (v^H v) */
+      double vv[MAXM], two[MAXM];
+      md_set_d(m, 1.0, vv);
+      for (int64_t i = 1; i < n; ++i) {
+        z_abs2(m, &vr[i * m], &vi[i * m], t);
+        md_add(m, vv, t, vv);
+      }
+      md_set_d(m, 2.0, two);
+      md_div(m, two, vv, beta);
+      /* columns c > j: w = v^H a_c, a_c -= beta v w */
+      for (int64_t c = j + 1; c < K; ++c) {
+        double wr[MAXM], wi[MAXM], pr2[MAXM], pi2[MAXM];
+        md_zero(m, wr);
+        md_zero(m, wi);
+        for (int64_t i = 0; i < n; ++i) {
+          z_cmul(m, &vr[i * m], &vi[i * m], FR(j + i, c), FI(j + i, c), pr2, pi2);
+          md_add(m, wr, pr2, wr);
+          md_add(m, wi, pi2, wi);
+        }
+        md_mul(m, beta, wr, wr);
+        md_mul(m, beta, wi, wi);
+        for (int64_t i = 0; i < n; ++i) {
+          z_mul(m, &vr[i * m], &vi[i * m], wr, wi, pr2, pi2);
+          md_sub(m, FR(j + i, c), pr2, FR(j + i, c));
+          md_sub(m, FI(j + i, c), pi2, FI(j + i, c));
+        }
+      }
+      /* y = H y on rows j.. (Q^H b, reflectors in order) */
+      {
+        double wr[MAXM], wi[MAXM], pr2[MAXM], pi2[MAXM];
+        md_zero(m, wr);
+        md_zero(m, wi);
+        for (int64_t i = 0; i < n; ++i) {
+          z_cmul(m, &vr[i * m], &vi[i * m], &yr[(j + i) * m], &yi[(j + i) * m], pr2, pi2);
+          md_add(m, wr, pr2, wr);
+          md_add(m, wi, pi2, wi);
+        }
+        md_mul(m, beta, wr, wr);
+        md_mul(m, beta, wi, wi);
+        for (int64_t i = 0; i < n; ++i) {
+          z_mul(m, &vr[i * m], &vi[i * m], wr, wi, pr2, pi2);
+          md_sub(m, &yr[(j + i) * m], pr2, &yr[(j + i) * m]);
+          md_sub(m, &yi[(j + i) * m], pi2, &yi[(j + i) * m]);
+        }
+      }
+      md_copy(m, ar, FR(j, j));
+      md_copy(m, ai, FI(j, j));
+      for (int64_t i = 1; i < n; ++i) {
+        md_zero(m, FR(j + i, j));
+        md_zero(m, FI(j + i, j));
+      }
+    }
+    if (md_lead(FR(j, j)) == 0.0 && md_lead(FI(j, j)) == 0.0 && !info) info = (int)(j + 1);
+  }
+  /* R x = y(1:K), complex back substitution */
+  for (int64_t i = K - 1; i >= 0; --i) {
+    double sr[MAXM], si[MAXM], pr2[MAXM], pi2[MAXM];
+    md_copy(m, &yr[i * m], sr);
+    md_copy(m, &yi[i * m], si);
+    for (int64_t l = i + 1; l < K; ++l) {
+      z_mul(m, FR(i, l), FI(i, l), &xr_[l * m], &xi_[l * m], pr2, pi2);
+      md_sub(m, sr, pr2, sr);
+      md_sub(m, si, pi2, si);
+    }
+    z_div(m, sr, si, FR(i, i), FI(i, i), &xr_[i * m], &xi_[i * m]);
+  }
+  for (int64_t i = 0; i < K; ++i)
+    for (int k = 0; k < m; ++k) {
+      xre[(int64_t)k * K + i] = xr_[i * m + k];
+      xim[(int64_t)k * K + i] = xi_[i * m + k];
+    }
+  if (Rre && Rim)
+    for (int64_t j = 0; j < K; ++j)
+      for (int64_t i = 0; i < M; ++i)
+        for (int k = 0; k < m; ++k) {
+          Rre[(int64_t)k * M * K + j * M + i] = (i <= j) ? FR(i, j)[k] : 0.0;
+          Rim[(int64_t)k * M * K + j * M + i] = (i <= j) ? FI(i, j)[k] : 0.0;
+        }
+#undef FR
+#undef FI
+  free(Fr);
+  free(Fi);
+  free(yr);
+  free(yi);
+  free(vr);
+  free(vi);
+  free(xr_);
+  free(xi_);
+  return info;
+}
+
 /* runtime self-check of round-to-nearest-even without reassociation:
  * two_sum(2^53, 1) must give (2^53, 1). */
 int oracle_selfcheck(void) {
