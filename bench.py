@@ -412,6 +412,8 @@ def run_ours(args, ws, rank, local):
                         f"{rb['groups']} stream groups (config 5b's per-GPU unit)",
             "ms_per_batch": round(rb["ms_per_step"], 3), "ms_per_solve": round(rb["ms_per_solve_per_gpu"], 4),
             "gflops": round(vb, 2), "fp64_peak_frac": round(vb / (FP64_PEAK_TFLOPS * 1e3), 4)}
+    if not args.no_extra and args.workload == "cfg2" and ws == 1:
+        res["complex_t5"] = bench_complex(dev, "dd", 512, 64, max(3, min(args.steps, 10)))
     if not args.no_extra and args.workload == "cfg2":
         res["backsub_cfg4"] = bench_backsub(dev, "qd", 17920, 128, max(3, min(args.steps, 10)), 2, args.no_graph)
     if rank == 0 and ws == 1 and not args.no_cpu:
@@ -524,6 +526,35 @@ def run_sharded_workload(args, ws, rank, dev, barrier, max_over_ranks):
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(res), flush=True)
+
+
+def bench_complex(dev, prec, n, nb, steps):
+    """Row f2 / T5's complex shape: complex least squares n x n (mdls_zlstsq, the real embedding solved by the
+    real pipeline), time per solve with CUDA events; flops = the ledger of the embedded 2n x 2n real solve."""
+    import torch
+
+    import paper_2110_08375_b200 as mdls
+    from paper_2110_08375_b200 import inputs
+
+    Are, bre = inputs.lstsq_problem(n, n, prec, 51)
+    Aim, bim = inputs.lstsq_problem(n, n, prec, 52)
+    t = [torch.from_numpy(a).to(dev) for a in (Are, Aim, bre, bim)]
+    work = torch.empty(mdls.workspace_bytes(prec, 5, n, n, nb), dtype=torch.uint8, device=dev)
+    for _ in range(2):
+        mdls.zlstsq(prec, *t, nb, work=work)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        _, _, info = mdls.zlstsq(prec, *t, nb, work=work)
+    e1.record()
+    torch.cuda.synchronize()
+    assert int(info.item()) == 0
+    ms = e0.elapsed_time(e1) / steps
+    f = ledger_flops(prec, 2 * n, 2 * n, nb)["total_flops"]
+    return {"workload": f"complex {prec} least squares {n}x{n}, tile {nb} (real embedding 2n x 2n, mdls_zlstsq)",
+            "ms_per_solve": round(ms, 4), "embedded_gflops": round(f / (ms * 1e-3) / 1e9, 2),
+            "paper_V100_complex_dd_512_ms_T5": "see BASELINE.md T5"}
 
 
 def bench_backsub(dev, prec, n, nb, steps, warmup, no_graph):

@@ -56,7 +56,8 @@ enum {
   MDLS_OP_BACKSUB = 1,   /* mdls_backsub_<p>                                       */
   MDLS_OP_LSTSQ = 2,     /* mdls_lstsq_<p>: QR + Q + Q^T b (explicit Q) + backsub  */
   MDLS_OP_APPLY_QT = 3,  /* mdls_apply_qt_<p>                                      */
-  MDLS_OP_LSTSQ_NOQ = 4  /* lstsq without forming Q (Q^T b applied from the panels) */
+  MDLS_OP_LSTSQ_NOQ = 4, /* lstsq without forming Q (Q^T b applied from the panels) */
+  MDLS_OP_ZLSTSQ = 5     /* mdls_zlstsq_<p>: complex least squares (M, K: the complex shape) */
 };
 
 /* stages of the flop ledger; the labels follow the paper's tables
@@ -207,6 +208,16 @@ int mdls_trace_collect(double *stage_ms, double *family_ms, int64_t *family_laun
                                   size_t work_bytes, int *dev_info, void **plan);                                  \
   /* bytes of `work` for mdls_lstsq_batched_<p> (op MDLS_OP_LSTSQ or MDLS_OP_LSTSQ_NOQ); 0 for invalid sizes. */ \
   size_t mdls_workspace_batched_##P(int op, int64_t M, int64_t K, int64_t nb, int groups);                        \
+                                                                                                                   \
+  /* complex least squares (row f2, re/im parts in separate limb-planar arrays):          \
+   * x = argmin ||b - A x||_2 for complex A (M x K: Are + i Aim, both (ptr, lda, psa)), b (bre + i bim, planes psb)\
+   * and x (xre + i xim, planes psx).  Solved through the real embedding [[Re A, -Im A], [Im A, Re A]] (2M x 2K)  \
+   * [Re x; Im x] = [Re b; Im b] -- the same minimiser, since ||b - Ax||^2 = ||Re(b - Ax)||^2 + ||Im(b - Ax)||^2 -- \
+   * by the real pipeline (mdls_lstsq, tile nb; 2K % nb == 0 required).  work: mdls_workspace_<p>(MDLS_OP_ZLSTSQ, \
+   * M, K, nb) bytes (form_q = 1) -- the embedded problem, its plan and the real solution. */                   \
+  int mdls_zlstsq_##P(int64_t M, int64_t K, int64_t nb, const double *Are, const double *Aim, int64_t lda,        \
+                      int64_t psa, const double *bre, const double *bim, int64_t psb, double *xre, double *xim,    \
+                      int64_t psx, int form_q, void *work, size_t work_bytes, int *dev_info, void *stream);         \
                                                                                                                    \
   /* ||y||_2 of the md vector y of length n (n >= 0), in md: one md number written to out (limb l at           \
    * out[l*pso]).  With y = (Q^T b)(K+1:M) from mdls_lstsq's y_out this is the least-squares residual norm        \

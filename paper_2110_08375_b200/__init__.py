@@ -232,6 +232,32 @@ def lstsq(prec: str, A, b, nb: int, form_q: bool = True, want_R: bool = False, w
     return LstsqResult(x, R, Q, y if want_y else None, info, res)
 
 
+def zlstsq(prec: str, Are, Aim, bre, bim, nb: int, form_q: bool = True, work=None):
+    """Complex least squares (mdls_zlstsq_<p>, row f2): A = Are + i Aim (m, K, M each), b = bre + i bim (m, M).
+    Returns (xre, xim, info)."""
+    torch = _torch()
+    for t, nm in ((Are, "Are"), (Aim, "Aim")):
+        _check_md(t, prec, 3, nm)
+    for t, nm in ((bre, "bre"), (bim, "bim")):
+        _check_md(t, prec, 2, nm)
+    m, K, M = Are.shape
+    if Aim.shape != Are.shape or bre.shape != (m, M) or bim.shape != (m, M):
+        raise ValueError("re/im shapes differ")
+    dev = Are.device
+    xre = torch.empty((m, K), dtype=torch.float64, device=dev)
+    xim = torch.empty((m, K), dtype=torch.float64, device=dev)
+    nbytes = int(_lib.fn("mdls_workspace_", prec)(_lib.OP_ZLSTSQ, M, K, nb))
+    if nbytes == 0:
+        raise ValueError("invalid complex least-squares shape (need M >= K, nb | 2K, nb <= 256)")
+    if work is None or work.numel() < nbytes:
+        work = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    info = _info(dev)
+    rc = _lib.fn("mdls_zlstsq_", prec)(M, K, nb, _ptr(Are), _ptr(Aim), M, K * M, _ptr(bre), _ptr(bim), M, _ptr(xre),
+                                       _ptr(xim), K, int(form_q), _ptr(work), work.numel(), _ptr(info), _stream())
+    _lib.check(rc, "zlstsq")
+    return xre, xim, info
+
+
 def batch_workspace_bytes(prec: str, op: int, M: int, K: int, nb: int, groups: int) -> int:
     return int(_lib.fn("mdls_workspace_batched_", prec)(op, M, K, nb, groups))
 

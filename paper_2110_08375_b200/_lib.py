@@ -15,7 +15,7 @@ PRECS = ("dd", "qd", "od")
 NSTAGES = 9
 STAGES = ("house", "panel", "wy", "trailing", "form_q", "qtb", "invert", "mulinv", "bsupdate")
 FAMILIES = ("gemm", "panel", "invert", "backsub", "other")
-OP_QR, OP_BACKSUB, OP_LSTSQ, OP_APPLY_QT, OP_LSTSQ_NOQ = 0, 1, 2, 3, 4
+OP_QR, OP_BACKSUB, OP_LSTSQ, OP_APPLY_QT, OP_LSTSQ_NOQ, OP_ZLSTSQ = 0, 1, 2, 3, 4, 5
 ERR_CUDA, ERR_UNSUPPORTED = -100, -101
 
 _P = ctypes.c_void_p
@@ -51,6 +51,7 @@ _SIGS = {
     "mdls_norm2_": (_I, [_L, _P, _L, _P, _L, _P]),
     "mdls_lstsq_batched_": (_I, [_L, _L, _L, _L, _P, _L, _L, _L, _P, _L, _L, _P, _L, _L, _I, _I, _P, _Z, _P, _P]),
     "mdls_workspace_batched_": (_Z, [_I, _L, _L, _L, _I]),
+    "mdls_zlstsq_": (_I, [_L, _L, _L, _P, _P, _L, _L, _P, _P, _L, _P, _P, _L, _I, _P, _Z, _P, _P]),
     "mdls_lstsq_plan_": (_I, [_L, _L, _L, _P, _L, _L, _P, _L, _P, _L, _I, _P, _Z, _P, ctypes.POINTER(_P)]),
     "mdls_lstsq_batched_plan_": (_I, [_L, _L, _L, _L, _P, _L, _L, _L, _P, _L, _L, _P, _L, _L, _I, _I, _P, _Z, _P,
                                       ctypes.POINTER(_P)]),

@@ -71,7 +71,20 @@ using namespace mdls::api_impl;
 
 extern "C" {
 
+// the complex problem's workspace: the real embedding (2M x 2K), its right-hand side and solution, then the
+// plan of the embedded real least-squares problem
+static size_t zplan_bytes(int64_t Mr, int64_t K, int64_t nb, int form_q, size_t* emb) {
+  const size_t md = sizeof(double) * M;
+  *emb = align256(md * 4 * Mr * K) + align256(md * 2 * Mr) + align256(md * 2 * K);
+  return *emb + make_plan<M>(form_q ? MDLS_OP_LSTSQ : MDLS_OP_LSTSQ_NOQ, 2 * Mr, 2 * K, nb).total;
+}
+
 size_t MDLS_FN(mdls_workspace_)(int op, int64_t Mr, int64_t K, int64_t nb) {
+  if (op == MDLS_OP_ZLSTSQ) {
+    if (tile_ok(2 * Mr, 2 * K, nb) || Mr < K) return 0;
+    size_t emb;
+    return zplan_bytes(Mr, K, nb, 1, &emb);
+  }
   if (op == MDLS_OP_BACKSUB) {
     if (K < 1 || nb < 1 || nb > 256 || K % nb) return 0;
     return make_plan<M>(op, K, K, nb).total;
@@ -275,6 +288,37 @@ int MDLS_FN(mdls_qt_b_)(int64_t Mr, int64_t Nc, const double* Q, int64_t ldq, in
   double* part = (work && work_bytes >= need) ? static_cast<double*>(work) : nullptr;
   gemm<M, true, false>(st, Nc, 1, Mr, CMat{Q, ldq, psq}, CMat{b, Mr, psb}, Mat{y, Nc, psy}, 0, part,
                        part ? kMaxSplit * Nc : 0);
+  return launched();
+}
+
+int MDLS_FN(mdls_zlstsq_)(int64_t Mr, int64_t K, int64_t nb, const double* Are, const double* Aim, int64_t lda,
+                          int64_t psa, const double* bre, const double* bim, int64_t psb, double* xre, double* xim,
+                          int64_t psx, int form_q, void* work, size_t work_bytes, int* dev_info, void* stream) {
+  if (Mr < K) return -1;
+  if (K < 1) return -2;
+  if (nb < 1 || nb > 256 || (2 * K) % nb) return -3;
+  if (!mat_ok(Are, Mr, K, lda, psa)) return -4;
+  if (!mat_ok(Aim, Mr, K, lda, psa)) return -5;
+  if (!bre || psb < Mr) return -8;
+  if (!bim) return -9;
+  if (!xre || psx < K) return -11;
+  if (!xim) return -12;
+  size_t emb;
+  if (!work || work_bytes < zplan_bytes(Mr, K, nb, form_q, &emb)) return -16;
+  cudaStream_t st = S(stream);
+  set_stage(MDLS_NSTAGES);
+  const size_t md = sizeof(double) * M;
+  double* E = static_cast<double*>(work);
+  double* eb = at<double>(work, align256(md * 4 * Mr * K));
+  double* ex = at<double>(work, align256(md * 4 * Mr * K) + align256(md * 2 * Mr));
+  const int64_t M2 = 2 * Mr, K2 = 2 * K;
+  MDLS_LAUNCH(F_MISC, st, embed_complex_kernel<M><<<grid_for(Mr * K, 256), 256, 0, st>>>(
+                              Mr, K, CMat{Are, lda, psa}, CMat{Aim, lda, psa}, bre, bim, psb, Mat{E, M2, M2 * K2}, eb, M2));
+  const int rc = lstsq_run(st, M2, K2, nb, E, M2, M2 * K2, eb, M2, ex, K2, form_q, nullptr, 0, 0, nullptr, 0, 0, nullptr,
+                           0, static_cast<char*>(work) + emb, dev_info);
+  if (rc) return rc;
+  MDLS_LAUNCH(F_MISC, st, copy_kernel<M><<<grid_for(K, 256), 256, 0, st>>>(K, 1, CMat{ex, K, K2}, Mat{xre, K, psx}, 0));
+  MDLS_LAUNCH(F_MISC, st, copy_kernel<M><<<grid_for(K, 256), 256, 0, st>>>(K, 1, CMat{ex + K, K, K2}, Mat{xim, K, psx}, 0));
   return launched();
 }
 

@@ -64,6 +64,29 @@ __global__ void copy_kernel(int64_t rows, int64_t cols, CMat src, Mat dst, int z
   }
 }
 
+// real embedding of a complex M x K matrix: E = [[Re, -Im], [Im, Re]] (2M x 2K, ld 2M) and of b: [Re b; Im b]
+template <int M>
+__global__ void embed_complex_kernel(int64_t rows, int64_t cols, CMat Ar, CMat Ai, const double* br,
+                                     const double* bi, int64_t psb, Mat E, double* eb, int64_t pse) {
+  const int64_t total = rows * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % rows, j = e / rows;
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+      const double re = Ar.p[k * Ar.ps + j * Ar.ld + i], im = Ai.p[k * Ai.ps + j * Ai.ld + i];
+      double* p = E.p + k * E.ps;
+      p[j * E.ld + i] = re;
+      p[j * E.ld + rows + i] = im;
+      p[(cols + j) * E.ld + i] = -im;
+      p[(cols + j) * E.ld + rows + i] = re;
+      if (j == 0) {
+        eb[k * pse + i] = br[k * psb + i];
+        eb[k * pse + rows + i] = bi[k * psb + i];
+      }
+    }
+  }
+}
+
 // explicit Y (unit lower trapezoidal) from a factored A: 0 above, 1 on, v below the diagonal
 template <int M>
 __global__ void extract_y_kernel(int64_t rows, int64_t cols, CMat a, Mat y) {
