@@ -568,7 +568,8 @@ __device__ __forceinline__ void leaf_prologue(const LeafArgs<M>& a, cg::cluster_
   LEAF_MARK(63, 0);
   cluster.sync();  // barriers armed everywhere, staging visible
   LEAF_MARK(63, 1);
-  // Z partial (p, c) over the staged rows, RS lanes per entry, 4 interleaved accumulators
+  // Z partial (p, c) over the staged rows, RS lanes per entry, 4 interleaved accumulators (od: 2, its
+  // operands loaded just in time -- four od accumulators and their operands do not fit the registers)
   {
     const int e = tid / RS, r0 = tid % RS;
     if (e < BB) {
@@ -576,20 +577,30 @@ __device__ __forceinline__ void leaf_prologue(const LeafArgs<M>& a, cg::cluster_
       Acc<M> acc[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) acc[u].init();
-#pragma unroll 2
-      for (int i = 4 * r0; i < Rxp; i += 4 * RS) {
-        md<M> yv[4], cv[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          yv[u] = Ys[(i + u) * BP + p];
-          cv[u] = Cs[(i + u) * BP + c];
+      if constexpr (M == 8) {
+#pragma unroll 1
+        for (int i = 2 * r0; i < Rxp; i += 2 * RS) {
+          acc[0].add_prod(Ys[i * BP + p], Cs[i * BP + c]);
+          acc[1].add_prod(Ys[(i + 1) * BP + p], Cs[(i + 1) * BP + c]);
         }
+      } else {
+#pragma unroll 2
+        for (int i = 4 * r0; i < Rxp; i += 4 * RS) {
+          md<M> yv[4], cv[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) acc[u].add_prod(yv[u], cv[u]);
+          for (int u = 0; u < 4; ++u) {
+            yv[u] = Ys[(i + u) * BP + p];
+            cv[u] = Cs[(i + u) * BP + c];
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) acc[u].add_prod(yv[u], cv[u]);
+        }
       }
       acc[0].merge(acc[1]);
-      acc[2].merge(acc[3]);
-      acc[0].merge(acc[2]);
+      if constexpr (M != 8) {
+        acc[2].merge(acc[3]);
+        acc[0].merge(acc[2]);
+      }
 #pragma unroll
       for (int d = RS / 2; d >= 1; d >>= 1) {
         Acc<M> o = acc_shfl_down<M>(acc[0], d);
@@ -650,7 +661,7 @@ __device__ __forceinline__ void leaf_prologue(const LeafArgs<M>& a, cg::cluster_
   mbar_wait(smem_addr(&zbar[1]), zpar);
   __syncthreads();
   LEAF_MARK(63, 5);
-  // update own rows (registers) and, in CTA 0, the B rows above the leaf (global)
+  // update own rows (registers) and the B rows above the leaf (global; row jsp + rank + k C on CTA rank)
   if (valid) {
     const int h = tid % TPR;
     const int i = ex + (int)(gi - row0);
@@ -659,27 +670,70 @@ __device__ __forceinline__ void leaf_prologue(const LeafArgs<M>& a, cg::cluster_
     for (int q = 0; q < V; ++q)
 #pragma unroll
       for (int k = 0; k < Acc<M>::NV; ++k) u[q].r(k) = (k < M) ? t[q].v[k] : 0.0;
-#pragma unroll 4
-    for (int p = 0; p < B; ++p) {
-      const md<M> y = neg(Ys[i * BP + p]);
+    if constexpr (M == 8) {
+      // two chains per column (even / odd terms), merged at the end: half the dependent od products
+      Acc<M> u2[V];
 #pragma unroll
-      for (int q = 0; q < V; ++q) u[q].add_prod(y, Zp[p * B + h * V + q]);
+      for (int q = 0; q < V; ++q) u2[q].init();
+#pragma unroll 1
+      for (int p = 0; p < B; p += 2) {
+        const md<M> y0 = neg(Ys[i * BP + p]), y1 = neg(Ys[i * BP + p + 1]);
+#pragma unroll
+        for (int q = 0; q < V; ++q) {
+          u[q].add_prod(y0, Zp[p * B + h * V + q]);
+          u2[q].add_prod(y1, Zp[(p + 1) * B + h * V + q]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < V; ++q) u[q].merge(u2[q]);
+    } else {
+#pragma unroll 4
+      for (int p = 0; p < B; ++p) {
+        const md<M> y = neg(Ys[i * BP + p]);
+#pragma unroll
+        for (int q = 0; q < V; ++q) u[q].add_prod(y, Zp[p * B + h * V + q]);
+      }
     }
 #pragma unroll
     for (int q = 0; q < V; ++q) t[q] = u[q].get();
   }
-  for (int e = tid; e < ex * B; e += NT) {
-    const int i = e / B, c = e % B;
-    Acc<M> u;
-    const md<M> c0 = Cs[i * BP + c];
+  if constexpr (M == 8) {
+    // od: each row above the leaf by the last warp, lane = (column c, term quarter), one or two products per
+    // lane merged over the quarters by shuffles -- instead of one thread per entry summing all B terms
+    static_assert(B <= 32 && 32 % B == 0, "od leaf width");
+    constexpr int NPART = 32 / B;
+    if (tid >= NT - 32) {
+      const int ln = tid & 31, c = ln % B, part = ln / B;
+      for (int i = 0; i < ex; ++i) {  // warp-uniform
+        Acc<M> u;
+        u.init();
+        if (part == 0) {
+          const md<M> c0 = Cs[i * BP + c];
 #pragma unroll
-    for (int k = 0; k < Acc<M>::NV; ++k) u.r(k) = (k < M) ? c0.v[k] : 0.0;
-    for (int p = 0; p < B; ++p) u.add_prod(neg(Ys[i * BP + p]), Zp[p * B + c]);
-    const md<M> r = u.get();
+          for (int k = 0; k < M; ++k) u.r(k) = c0.v[k];
+        }
+        for (int p = part; p < B; p += NPART) u.add_prod(neg(Ys[i * BP + p]), Zp[p * B + c]);
 #pragma unroll
-    if (c < ncols)
+        for (int d = B; d < 32; d <<= 1) u.merge(acc_shfl_xor<M>(u, d));
+        const md<M> r = u.get();
+        if (part == 0 && c < ncols)
 #pragma unroll
-      for (int k = 0; k < M; ++k) a.A.p[k * a.A.ps + (a.js + c) * a.A.ld + a.jsp + rank + (int64_t)i * C] = r.v[k];
+          for (int k = 0; k < M; ++k) a.A.p[k * a.A.ps + (a.js + c) * a.A.ld + a.jsp + rank + (int64_t)i * C] = r.v[k];
+      }
+    }
+  } else {
+    for (int e = tid; e < ex * B; e += NT) {
+      const int i = e / B, c = e % B;
+      Acc<M> u;
+      const md<M> c0 = Cs[i * BP + c];
+#pragma unroll
+      for (int k = 0; k < Acc<M>::NV; ++k) u.r(k) = (k < M) ? c0.v[k] : 0.0;
+      for (int p = 0; p < B; ++p) u.add_prod(neg(Ys[i * BP + p]), Zp[p * B + c]);
+      const md<M> r = u.get();
+      if (c < ncols)
+#pragma unroll
+        for (int k = 0; k < M; ++k) a.A.p[k * a.A.ps + (a.js + c) * a.A.ld + a.jsp + rank + (int64_t)i * C] = r.v[k];
+    }
   }
   LEAF_MARK(63, 6);
   (void)lane;
