@@ -47,7 +47,7 @@ FP64_PIPE_TOPS = 148 * 64 * 1.965e9 / 1e12            # 18.6 FP64-pipe lane ops/
 # FP64 pipe instructions per md pair (one md mul + one md add) as the GEMM kernels implement them
 # (md.cuh Acc: dd unnormalised FMA pair accumulation 12; qd/od level-bin accumulation: 2M-1 FMAs +
 # sum_{n<=M-2} (n+1) [two_prod + exact deposits] = 115 / 967, + the per-k-tile bin renormalisation)
-OPS_PER_PAIR = {"dd": 12, "qd": 116, "od": 970}
+OPS_PER_PAIR = {"d": 1, "dd": 12, "qd": 116, "od": 970}
 # dram traffic per launch of the roofline GEMM (1024 x 1024 x 128, C += X Y^T) from one ncu --set full
 # capture (tools/prof_gemm.py; dd: profiles/r02_ncu_final.txt, stream-K; qd/od: profiles/r01_ncu_gemm_roofline.txt)
 GEMM_NCU_TRAFFIC = {"dd": 21080064 + 23296, "qd": 42001664 + 119040, "od": 84171776 + 14920192}
@@ -164,7 +164,7 @@ def gemm_roofline(dev, prec, M, nb, reps=20, warmup=3):
     import paper_2110_08375_b200 as mdls
     from paper_2110_08375_b200 import inputs
 
-    m_l = {"dd": 2, "qd": 4, "od": 8}[prec]
+    m_l = {"d": 1, "dd": 2, "qd": 4, "od": 8}[prec]
     X = torch.from_numpy(inputs.random_matrix(M, nb, prec, seed=11)).to(dev)
     Y = torch.from_numpy(inputs.random_matrix(M, nb, prec, seed=12)).to(dev)
     C = torch.from_numpy(inputs.random_matrix(M, M, prec, seed=13)).to(dev)
@@ -396,6 +396,13 @@ def run_ours(args, ws, rank, local):
                         "gflops": round(f / (r["ms_per_step"] * 1e-3) / 1e9, 2),
                         "fp64_peak_frac": round(f / (r["ms_per_step"] * 1e-3) / 1e12 / FP64_PEAK_TFLOPS, 4),
                         "speedup_vs_V100_kernel_time": round(PAPER_V100_MS[p] / r["ms_per_step"], 1)}
+        # plain double ("1d"): the paper lists its timings beside the md runs but does not compare them
+        # (P:599-604); flops = the same ledger counts at one flop per operation
+        r = measure("d", M, K, nb, max(3, min(args.steps, 10)), 1, seed=rank, with_e2e=False, with_trace=False)
+        f = ledger_flops("d", M, K, nb)["total_flops"]
+        extra["d"] = {"ms_per_solve": round(r["ms_per_step"], 4),
+                      "gflops": round(f / (r["ms_per_step"] * 1e-3) / 1e9, 2),
+                      "note": "plain double, same kernels with one limb; listed, not compared (P:599-604)"}
         res["precisions"] = extra
         res["overhead"] = {
             "dd_to_qd": round(extra["qd"]["ms_per_solve"] / extra["dd"]["ms_per_solve"], 2),

@@ -8,8 +8,12 @@
  * QR of Algorithm 2, R x = y from the tiled accelerated back
  * substitution of Algorithm 1.
  *
- * PRECISIONS.  Every compute entry point exists three times, suffix _dd, _qd,
- * _od: double double, quad double, octo double = m = 2, 4, 8 limbs.
+ * PRECISIONS.  Every compute entry point exists four times, suffix _dd, _qd,
+ * _od: double double, quad double, octo double = m = 2, 4, 8 limbs,
+ * and _d: plain IEEE double (m = 1), the paper's "double precision version"
+ * whose timings are listed beside the md runs.  _d runs the same
+ * algorithms and kernels with one rounded operation per md operation (products
+ * accumulated by FMA); its ledger prices every operation at one flop.
  *
  * LAYOUT ("staggered").  An md matrix is m plain double matrices,
  * most significant first.  Every matrix operand is described by
@@ -91,7 +95,7 @@ typedef struct {
 const char *mdls_strerror(int code);
 int mdls_version(void);
 /* number of limbs of each precision */
-int mdls_limbs(int prec_index /* 0 dd, 1 qd, 2 od */);
+int mdls_limbs(int prec_index /* 0 dd, 1 qd, 2 od, 3 d (plain double) */);
 
 /* Instrumentation (host side, process wide).
  * mdls_launch_count: kernels launched by the library since it was loaded.
@@ -244,6 +248,7 @@ int mdls_trace_collect(double *stage_ms, double *family_ms, int64_t *family_laun
 MDLS_DECLARE(dd)
 MDLS_DECLARE(qd)
 MDLS_DECLARE(od)
+MDLS_DECLARE(d)
 
 #undef MDLS_DECLARE
 

@@ -31,7 +31,7 @@ _SRC = os.path.join(_HERE, "mdls_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 _LIB_COUNT = os.path.join(_HERE, "liboracle_count.so")
 
-PRECISIONS = {"dd": 2, "qd": 4, "od": 8}
+PRECISIONS = {"d": 1, "dd": 2, "qd": 4, "od": 8}  # "d": plain double
 OPS = {"add": 0, "sub": 1, "mul": 2, "div": 3, "sqrt": 4}
 
 _CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-std=c11", "-Wall",

@@ -8,7 +8,9 @@
  *
  * What it computes (PAPER.md = arXiv 2110.08375, cited as P:<line>):
  *   - multiple double numbers: unevaluated sums of m doubles, m = 2 (dd), 4 (qd),
- *     8 (od).  Arithmetic is the paper's named families: QDlib for dd
+ *     8 (od); m = 1 is plain IEEE double arithmetic (one rounded
+ *     +,-,*,/,sqrt per operation), the paper's "double precision version" whose
+ *     timings are listed beside the md runs.  Arithmetic is the paper's named families: QDlib for dd
  *      and CAMPARY's generated qd/od code (P:152-156,
  *     P:615-625).  The paper prints no algorithm, only their Table 1 operation
  *     counts; the exact variants below are the readings of DESIGN.md
@@ -39,6 +41,8 @@
 #endif
 
 #define MAXM 8
+/* m = 1 is plain IEEE double ("1d", the paper's reference rows) */
+#define BAD_M(m) ((m) != 1 && (m) != 2 && (m) != 4 && (m) != 8)
 
 /* ------------------------------------------------------------------------- */
 /* base double operations, optionally counted                                 */
@@ -320,16 +324,20 @@ static void mdg_sqrt(int m, const double *a, double *c) {
 /* precision dispatch                                                         */
 /* ------------------------------------------------------------------------- */
 static void md_add(int m, const double *a, const double *b, double *c) {
-  if (m == 2) dd_add(a, b, c); else mdg_add(m, a, b, c);
+  if (m == 1) c[0] = ADD(a[0], b[0]);
+  else if (m == 2) dd_add(a, b, c); else mdg_add(m, a, b, c);
 }
 static void md_mul(int m, const double *a, const double *b, double *c) {
-  if (m == 2) dd_mul(a, b, c); else mdg_mul(m, a, b, c);
+  if (m == 1) c[0] = MUL(a[0], b[0]);
+  else if (m == 2) dd_mul(a, b, c); else mdg_mul(m, a, b, c);
 }
 static void md_div(int m, const double *a, const double *b, double *c) {
-  if (m == 2) dd_div(a, b, c); else mdg_div(m, a, b, c);
+  if (m == 1) c[0] = DIV(a[0], b[0]);
+  else if (m == 2) dd_div(a, b, c); else mdg_div(m, a, b, c);
 }
 static void md_sqrt(int m, const double *a, double *c) {
-  if (m == 2) dd_sqrt(a, c); else mdg_sqrt(m, a, c);
+  if (m == 1) c[0] = sqrt(a[0]); /* correctly rounded (IEEE 754) */
+  else if (m == 2) dd_sqrt(a, c); else mdg_sqrt(m, a, c);
 }
 static void md_neg(int m, const double *a, double *c) {
   for (int k = 0; k < m; ++k) c[k] = NEG(a[k]);
@@ -356,7 +364,7 @@ static int md_lt(int m, const double *a, const double *b) {
 
 /* vectorised single-operation entry point (op: 0 add, 1 sub, 2 mul, 3 div, 4 sqrt) */
 int oracle_md_op(int op, int m, int64_t n, const double *a, const double *b, double *c) {
-  if (m != 2 && m != 4 && m != 8) return -2;
+  if (BAD_M(m)) return -2;
   for (int64_t i = 0; i < n; ++i) {
     double x[MAXM], y[MAXM], z[MAXM];
     for (int k = 0; k < m; ++k) {
@@ -377,7 +385,7 @@ int oracle_md_op(int op, int m, int64_t n, const double *a, const double *b, dou
 }
 /* renormalisation of an (m+1)-term array, for the renorm pins */
 int oracle_renorm(int m, const double *f, double *r) {
-  if (m != 2 && m != 4 && m != 8) return -2;
+  if (BAD_M(m)) return -2;
   renorm(m, f, r);
   return 0;
 }
@@ -449,7 +457,7 @@ static void house(int m, int64_t n, const double *x, double *v, double *beta, do
 }
 
 int oracle_house(int m, int64_t n, const double *x_planes, double *v_planes, double *beta, double *mu) {
-  if (m != 2 && m != 4 && m != 8) return -2;
+  if (BAD_M(m)) return -2;
   double *x = malloc(sizeof(double) * m * n), *v = malloc(sizeof(double) * m * n);
   for (int64_t i = 0; i < n; ++i)
     for (int k = 0; k < m; ++k) x[i * m + k] = x_planes[k * n + i];
@@ -468,7 +476,7 @@ int oracle_house(int m, int64_t n, const double *x_planes, double *v_planes, dou
 /* beta: m planes of K.  Every dot product accumulates from 0 ascending.       */
 /* ------------------------------------------------------------------------- */
 int oracle_qr(int m, int64_t M, int64_t K, double *Ap, int64_t lda, double *beta_p, int nthreads) {
-  if (m != 2 && m != 4 && m != 8) return -2;
+  if (BAD_M(m)) return -2;
   if (M < K || K < 0 || lda < M) return -1;
   set_threads(nthreads);
   mat_t A = {Ap, lda, K, m};
@@ -517,7 +525,7 @@ static void load_v(const mat_t *A, int64_t M, int64_t j, double *v) {
  * Q(j:M, c) -= beta_j (v_j . Q(j:M, c)) v_j for the columns c >= j. */
 int oracle_form_q(int m, int64_t M, int64_t K, const double *Ap, int64_t lda, const double *beta_p, double *Qp,
                   int64_t ldq, int nthreads) {
-  if (m != 2 && m != 4 && m != 8) return -2;
+  if (BAD_M(m)) return -2;
   if (M < K || ldq < M || lda < M) return -1;
   set_threads(nthreads);
   mat_t A = {(double *)Ap, lda, K, m};
@@ -556,7 +564,7 @@ int oracle_form_q(int m, int64_t M, int64_t K, const double *Ap, int64_t lda, co
  * y(j:M) -= beta_j (v_j . y(j:M)) v_j. */
 int oracle_apply_qt(int m, int64_t M, int64_t K, const double *Ap, int64_t lda, const double *beta_p,
                     const double *b, double *y) {
-  if (m != 2 && m != 4 && m != 8) return -2;
+  if (BAD_M(m)) return -2;
   mat_t A = {(double *)Ap, lda, K, m};
   mat_t Y = {y, M, 1, m};
   if (y != b) memcpy(y, b, sizeof(double) * m * M);
@@ -587,7 +595,7 @@ int oracle_apply_qt(int m, int64_t M, int64_t K, const double *Ap, int64_t lda, 
 /* y = Q^T b with an explicit Q (y_c = sum_i Q(i,c) b_i, ascending i). */
 int oracle_qt_b_explicit(int m, int64_t M, const double *Qp, int64_t ldq, const double *b, double *y,
                          int nthreads) {
-  if (m != 2 && m != 4 && m != 8) return -2;
+  if (BAD_M(m)) return -2;
   set_threads(nthreads);
   mat_t Q = {(double *)Qp, ldq, M, m};
   mat_t B = {(double *)b, M, 1, m};
@@ -614,7 +622,7 @@ int oracle_qt_b_explicit(int m, int64_t M, const double *Qp, int64_t ldq, const 
  * Returns 0, or i+1 (1-based) for the first zero diagonal met. */
 int oracle_backsub(int m, int64_t n, const double *Rp, int64_t ldr, int64_t rcols, const double *y, int64_t ylen,
                    double *x) {
-  if (m != 2 && m != 4 && m != 8) return -2;
+  if (BAD_M(m)) return -2;
   mat_t R = {(double *)Rp, ldr, rcols, m};
   double *xx = malloc(sizeof(double) * m * (n + 1));
   int info = 0;
@@ -640,7 +648,7 @@ int oracle_backsub(int m, int64_t n, const double *Rp, int64_t ldr, int64_t rcol
  * planes pa / pb apart, strides sa / sb between entries) */
 int oracle_dot(int m, int64_t n, const double *a, int64_t pa, int64_t sa, const double *b, int64_t pb, int64_t sb,
                double *out) {
-  if (m != 2 && m != 4 && m != 8) return -2;
+  if (BAD_M(m)) return -2;
   double s[MAXM], t[MAXM], x[MAXM], y[MAXM];
   md_zero(m, s);
   for (int64_t i = 0; i < n; ++i) {
@@ -658,7 +666,7 @@ int oracle_dot(int m, int64_t n, const double *a, int64_t pa, int64_t sa, const 
 /* ||y||_2 in md: s = sum_i y_i^2 ascending from 0, then md sqrt (the residual norm of SPEC S:448 when
  * y = (Q^T b)(K+1:M)) */
 int oracle_norm2(int m, int64_t n, const double *y, int64_t psy, double *out) {
-  if (m != 2 && m != 4 && m != 8) return -2;
+  if (BAD_M(m)) return -2;
   double s[MAXM], t[MAXM], v[MAXM];
   md_zero(m, s);
   for (int64_t i = 0; i < n; ++i) {
@@ -673,7 +681,7 @@ int oracle_norm2(int m, int64_t n, const double *y, int64_t psy, double *out) {
 /* ||b - A x||_2 in md, evaluated directly: r_i = b_i - sum_j A_ij x_j (ascending j), then oracle_norm2 */
 int oracle_residual_direct(int m, int64_t M, int64_t K, const double *Ap, int64_t lda, const double *x,
                            const double *b, double *out) {
-  if (m != 2 && m != 4 && m != 8) return -2;
+  if (BAD_M(m)) return -2;
   mat_t A = {(double *)Ap, lda, K, m};
   double *r = malloc(sizeof(double) * m * M);
   for (int64_t i = 0; i < M; ++i) {
@@ -697,7 +705,7 @@ int oracle_residual_direct(int m, int64_t M, int64_t K, const double *Ap, int64_
 /* ------------------------------------------------------------------------- */
 int oracle_lstsq(int m, int64_t M, int64_t K, const double *Ap, int64_t lda, const double *b, double *x,
                  double *R_out, double *y_out, int nthreads) {
-  if (m != 2 && m != 4 && m != 8) return -2;
+  if (BAD_M(m)) return -2;
   double *F = malloc(sizeof(double) * m * M * K);
   for (int k = 0; k < m; ++k)
     for (int64_t j = 0; j < K; ++j)
@@ -1119,7 +1127,7 @@ static int blocked_backsub(int m, int64_t n, int64_t nb, const mat_t *U, const d
  * Returns 0, a 1-based zero-diagonal row, or -1 for invalid arguments. */
 int oracle_blocked(int op, int m, int64_t M, int64_t K, int64_t nb, const double *A, const double *b, double *x,
                    double *R_out, double *Q_out, double *y_out, int64_t *counts, int64_t *nonpos) {
-  if (m != 2 && m != 4 && m != 8) return -1;
+  if (BAD_M(m)) return -1;
   if (nb < 1 || K < 1 || K % nb || (op != 1 && M < K) || op < 0 || op > 4) return -1;
   memset(g_mdc, 0, sizeof(g_mdc));
   int64_t np = 0;
@@ -1274,7 +1282,7 @@ static void z_div(int m, const double *ar, const double *ai, const double *br, c
 
 int oracle_zlstsq(int m, int64_t M, int64_t K, const double *Are, const double *Aim, int64_t lda, const double *bre,
                   const double *bim, double *xre, double *xim, double *Rre, double *Rim) {
-  if (m != 2 && m != 4 && m != 8) return -2;
+  if (BAD_M(m)) return -2;
   if (M < K || K < 1) return -3;
   /* working copies, element-major (m limbs contiguous): F(i, j) at ((j * M + i) * m) */
   double *Fr = malloc(sizeof(double) * m * M * K), *Fi = malloc(sizeof(double) * m * M * K);

@@ -15,10 +15,10 @@ import ctypes
 
 from . import _lib
 
-PRECISIONS = {"dd": 2, "qd": 4, "od": 8}
+PRECISIONS = {"dd": 2, "qd": 4, "od": 8, "d": 1}  # "d": plain double
 OPS = {"add": 0, "sub": 1, "mul": 2, "div": 3, "sqrt": 4, "sqrt_fast": 5, "recip_fast": 6, "wmul": 7, "wsqrt_fast": 8,
        "wrecip_fast": 9}
-T1_SUMS = {"dd": (20, 23, 70), "qd": (89, 336, 893), "od": (269, 1742, 5126)}  # P:102-136 (add, mul, div)
+T1_SUMS = {"dd": (20, 23, 70), "qd": (89, 336, 893), "od": (269, 1742, 5126), "d": (1, 1, 1)}  # P:102-136 (add, mul, div)
 
 __all__ = ["md_op", "qr", "apply_qt", "qt_b", "invert_tiles", "backsub", "lstsq", "norm2", "counts",
            "workspace_bytes", "PRECISIONS"]

@@ -11,7 +11,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libmdls.so")
 
-PRECS = ("dd", "qd", "od")
+PRECS = ("dd", "qd", "od", "d")
 NSTAGES = 9
 STAGES = ("house", "panel", "wy", "trailing", "form_q", "qtb", "invert", "mulinv", "bsupdate")
 FAMILIES = ("gemm", "panel", "invert", "backsub", "other")

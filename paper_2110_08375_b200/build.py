@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libmdls.so")
-SOURCES = [f"{k}_{p}.cu" for p in ("od", "qd", "dd") for k in ("panel", "leafsm", "gemm", "bs", "api")] + ["ledger.cu"]
+SOURCES = [f"{k}_{p}.cu" for p in ("od", "qd", "dd", "d") for k in ("panel", "leafsm", "gemm", "bs", "api")] + ["ledger.cu"]
 HEADERS = ["md.cuh", "md_warp.cuh", "types.cuh", "launch.cuh", "kern_misc.cuh", "kern_gemm.cuh", "kern_leaf.cuh", "kern_bs.cuh",
            "solver.cuh", "api.cuh"]
 

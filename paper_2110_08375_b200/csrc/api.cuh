@@ -39,7 +39,7 @@ inline bool q_forward() {
     const char* e = getenv("MDLS_QFORM");
     if (e && e[0] == 'f') v = 1;
     else if (e && e[0] == 'b') v = 0;
-    else v = (MM == 2) ? 1 : 0;
+    else v = (MM <= 2) ? 1 : 0;
   }
   return v == 1;
 }
@@ -123,7 +123,7 @@ int MDLS_FN(mdls_invert_tiles_)(int64_t n, int64_t nb, const double* U, int64_t 
   } else {
     return -9;
   }
-  launch_invert<M>(st, n / nb, nb, CMat{U, ldu, psu}, Mat{Vt, ldv, psv}, Mat{nullptr, 0, 0}, slot);
+  launch_invert<M>(st, n / nb, nb, CMat{U, ldu, psu}, Mat{Vt, ldv, psv}, Mat{nullptr, 0, 0}, slot, 0);
   MDLS_LAUNCH(F_MISC, st, info_finish_kernel<<<1, 1, 0, st>>>(slot, nullptr, dev_info));
   return launched();
 }

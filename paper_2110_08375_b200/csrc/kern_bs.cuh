@@ -18,22 +18,25 @@ namespace mdls {
 // s_i -= u'_il x_l, whose U' loads are issued one step ahead).  Without it
 // (mdls_invert_tiles, no workspace) every step multiplies by 1/u_ll.
 // ============================================================================
-// Us(i, tile*nb + l) = u_il / u_ii for i < l, 1 / u_ll on the diagonal (one CTA per tile)
+// Us(i, tile*nb + l) = u_il / u_ii for i < l, 1 / u_ll on the diagonal.  Grid (tile, column slice):
+// every CTA forms the tile's nb reciprocal diagonal entries (cheap, nb md divisions spread over the
+// threads) and scales its own slice of columns, so a chunk of tiles fills the SMs.
 template <int M>
-__global__ void __launch_bounds__(256) scale_tiles_kernel(int64_t nb, CMat U, Mat Us, int* info) {
+__global__ void __launch_bounds__(256) scale_tiles_kernel(int64_t nb, CMat U, Mat Us, int* info, int64_t info_off) {
   extern __shared__ double smem_inv[];  // rinv: M planes of nb
   const int64_t base = (int64_t)blockIdx.x * nb;
+  const int64_t c0 = nb * blockIdx.y / gridDim.y, c1 = nb * (blockIdx.y + 1) / gridDim.y;
   for (int64_t r = threadIdx.x; r < nb; r += blockDim.x) {
     const md<M> d = ld<M>(U.p, U.ps, (base + r) + (base + r) * U.ld);
-    if (!(d.v[0] != 0.0) || !isfinite(d.v[0])) atomicMin(info, (int)(base + r + 1));
+    if (blockIdx.y == 0 && (!(d.v[0] != 0.0) || !isfinite(d.v[0]))) atomicMin(info, (int)(info_off + base + r + 1));
     const md<M> q = div<M>(md_from<M>(1.0), d);
 #pragma unroll
     for (int l = 0; l < M; ++l) smem_inv[l * nb + r] = q.v[l];
-    st<M>(Us.p, Us.ps, r + (base + r) * Us.ld, q);
+    if (r >= c0 && r < c1) st<M>(Us.p, Us.ps, r + (base + r) * Us.ld, q);
   }
   __syncthreads();
-  for (int64_t e = threadIdx.x; e < nb * nb; e += blockDim.x) {
-    const int64_t i = e % nb, l = e / nb;  // consecutive threads walk a column: coalesced
+  for (int64_t e = threadIdx.x; e < nb * (c1 - c0); e += blockDim.x) {
+    const int64_t i = e % nb, l = c0 + e / nb;  // consecutive threads walk a column: coalesced
     if (i >= l) continue;
     md<M> ri;
 #pragma unroll
@@ -43,7 +46,8 @@ __global__ void __launch_bounds__(256) scale_tiles_kernel(int64_t nb, CMat U, Ma
 }
 
 template <int M, int NPL, bool SCALED>
-__global__ void __launch_bounds__(256) invert_tiles_kernel(int64_t nb, CMat U, CMat Us, Mat Vt, int* info) {
+__global__ void __launch_bounds__(256) invert_tiles_kernel(int64_t nb, CMat U, CMat Us, Mat Vt, int* info,
+                                                           int64_t info_off) {
   extern __shared__ double smem_inv[];  // rinv: M planes of nb (unscaled path)
   const int tile = blockIdx.x;
   const int64_t base = (int64_t)tile * nb;  // tile rows/cols offset
@@ -52,7 +56,7 @@ __global__ void __launch_bounds__(256) invert_tiles_kernel(int64_t nb, CMat U, C
   if constexpr (!SCALED) {
     for (int64_t r = tid; r < nb; r += blockDim.x) {
       const md<M> d = ld<M>(U.p, U.ps, (base + r) + (base + r) * U.ld);
-      if (!(d.v[0] != 0.0) || !isfinite(d.v[0])) atomicMin(info, (int)(base + r + 1));
+      if (!(d.v[0] != 0.0) || !isfinite(d.v[0])) atomicMin(info, (int)(info_off + base + r + 1));
       const md<M> q = div<M>(md_from<M>(1.0), d);
 #pragma unroll
       for (int l = 0; l < M; ++l) smem_inv[l * nb + r] = q.v[l];
@@ -104,12 +108,14 @@ __global__ void __launch_bounds__(256) invert_tiles_kernel(int64_t nb, CMat U, C
       md<M> uc[NPL];
 #pragma unroll
       for (int t = 0; t < NPL; ++t) {
+        if (32 * t >= l) break;  // warp-uniform: row blocks at or below the pivot hold no work
         uc[t] = un[t];
         const int64_t i = lane + 32 * t;
         un[t] = (l >= 1 && i < l - 1) ? u_at(i, l - 1) : md_zero<M>();  // next step's column, in flight
       }
 #pragma unroll
       for (int t = 0; t < NPL; ++t) {
+        if (32 * t >= l) break;
         const int64_t i = lane + 32 * t;
         if (i < l) s[t].add_prod(uc[t], nx);
       }
@@ -122,20 +128,37 @@ __global__ void __launch_bounds__(256) invert_tiles_kernel(int64_t nb, CMat U, C
 // ============================================================================
 // A8: x_i = U_i^-1 b_i, one warp per output row (lanes over the columns)
 // ============================================================================
-template <int M>
+template <int M, int NPL>
 __global__ void __launch_bounds__(256) bs_mulinv_kernel(int64_t nb, int64_t tile, CMat Vt, const double* b,
                                                         int64_t psb, double* x, int64_t psx) {
+  pdl_trigger();
   const int lane = threadIdx.x & 31;
   const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (r >= nb) return;
   const int64_t base = tile * nb;
-  Acc<M> acc;
-  acc.init();
-  for (int64_t c = r + lane; c < nb; c += 32) {  // upper triangular: c >= r
-    md<M> t = ld<M>(Vt.p, Vt.ps, c + (base + r) * Vt.ld);
-    md<M> bb = ld<M>(b, psb, base + c);
-    acc.add_prod(t, bb);
+  // the lane's columns c = r + lane + 32 t (upper triangular: c >= r), every load issued before any product;
+  // the inverse (complete: a full dependency) before the PDL wait, b (the predecessor's output) after it
+  md<M> tv[NPL], bv[NPL];
+#pragma unroll
+  for (int t = 0; t < NPL; ++t) {
+    const int64_t c = r + lane + 32 * t;
+    tv[t] = (r < nb && c < nb) ? ld<M>(Vt.p, Vt.ps, c + (base + r) * Vt.ld) : md_zero<M>();
   }
+  pdl_wait();
+  if (r >= nb) return;
+#pragma unroll
+  for (int t = 0; t < NPL; ++t) {
+    const int64_t c = r + lane + 32 * t;
+    bv[t] = (c < nb) ? ld<M>(b, psb, base + c) : md_zero<M>();
+  }
+  Acc<M> acc, acc2;  // two independent chains (even / odd t), merged before the tree
+  acc.init();
+  acc2.init();
+#pragma unroll
+  for (int t = 0; t < NPL; t += 2) {
+    acc.add_prod(tv[t], bv[t]);
+    if (t + 1 < NPL) acc2.add_prod(tv[t + 1], bv[t + 1]);
+  }
+  acc.merge(acc2);
   // fixed-order tree of exact accumulator merges (no renormalised md add per level)
 #pragma unroll
   for (int d = 16; d >= 1; d >>= 1) acc.merge(acc_shfl_down<M>(acc, d));
@@ -144,96 +167,168 @@ __global__ void __launch_bounds__(256) bs_mulinv_kernel(int64_t nb, int64_t tile
 
 // ============================================================================
 // A9: b(rho) -= sum_c U(rho, tile*nb + c) x_tile(c) for rho in [row0, row1).
-// CTA = 32*RPT rows x G column groups: each thread keeps RPT independent row
-// accumulators over the columns c = g, g+G, ... (coalesced column reads of U),
-// then a fixed-order smem reduction over the G groups.
+// CTA = RB rows x (256 / RB) column groups: thread (r, g) owns row rb + r and, in
+// every stage, the stage's columns g, g + 256/RB, ...  The CTA's RB x nb block of
+// U streams through shared memory in stages of 2048 doubles (SC = 2048 / (M RB)
+// columns x M limb planes x RB rows) by cp.async (LDGSTS), NS - 1 stages in
+// flight, so the HBM latency overlaps the md arithmetic with no register staging;
+// x_tile is staged once per CTA; two accumulator chains per thread (alternate
+// columns).  Then a fixed-order smem tree over the column groups.
+// RB = 32 for the wide steps; RB = 8 spreads a short step over 4x the SMs.
+// Coalesced: consecutive threads copy consecutive rows of one column plane.
 // ============================================================================
-template <int M, int G, int RPT>
-__global__ void __launch_bounds__(32 * G) bs_update_kernel(int64_t nb, int64_t tile, int64_t row0, int64_t row1, CMat U,
+template <int M, int RB, int NS, int MINB, int NACC>
+__global__ void __launch_bounds__(256, MINB) bs_update_kernel(int64_t nb, int64_t tile, int64_t row0, int64_t row1, CMat U,
                                                            const double* x, int64_t psx, double* b, int64_t psb) {
-  __shared__ Acc<M> part[G][32 * RPT];
-  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
-  const int64_t rbase = row0 + (int64_t)blockIdx.x * 32 * RPT;
-  const int64_t base = tile * nb;
-  Acc<M> acc[RPT];
+  constexpr int NT = 256, GR = NT / RB, STAGE = 2048, SC = STAGE / (M * RB);
+  static_assert(SC >= GR && SC % GR == 0, "stage shape");
+  extern __shared__ double sm_bs[];
+  double* xs = sm_bs;              // M planes of nb: x_tile
+  double* ring = sm_bs + M * nb;   // NS stages of [limb][column][row]
+  __shared__ Acc<M> part[GR][RB];
+  const int tid = threadIdx.x, r = tid % RB, gq = tid / RB;
+  const int64_t base = tile * nb, rb = row0 + (int64_t)blockIdx.x * RB;
+  const int nst = (int)((nb + SC - 1) / SC);
+  auto issue = [&](int st) {
+    if (st < nst) {
+      double* dst = ring + (st % NS) * STAGE;
+      for (int e = tid; e < STAGE; e += NT) {
+        const int rr = e % RB, c = (e / RB) % SC, k = e / (RB * SC);
+        const int64_t col = (int64_t)st * SC + c, row = rb + rr;
+        const bool ok = col < nb && row < row1;
+        cp_async8(dst + e, ok ? U.p + k * U.ps + (base + col) * U.ld + row : U.p, ok);
+      }
+    }
+    cp_async_commit();  // one group per stage, empty past the end (uniform wait counts)
+  };
+  pdl_trigger();
 #pragma unroll
-  for (int t = 0; t < RPT; ++t) acc[t].init();
-  for (int64_t c = g; c < nb; c += G) {
-    const md<M> xx = ld<M>(x, psx, base + c);
+  for (int st = 0; st < NS - 1; ++st) issue(st);  // U is read-only here: prefetched before the PDL wait
+  pdl_wait();                                     // x (mulinv) and b (the previous update) from here on
+  for (int64_t e = tid; e < nb; e += NT)
 #pragma unroll
-    for (int t = 0; t < RPT; ++t) {
-      const int64_t rho = rbase + lane + 32 * t;
-      if (rho < row1) acc[t].add_prod(ld<M>(U.p, U.ps, rho + (base + c) * U.ld), xx);
+    for (int k = 0; k < M; ++k) xs[k * nb + e] = x[k * psx + base + e];
+  constexpr int CPT = SC / GR;  // columns per thread per stage
+  Acc<M> acc0, acc1;             // two independent chains (alternate columns), merged at the end
+  acc0.init();
+  acc1.init();
+  for (int st = 0; st < nst; ++st) {
+    cp_async_wait<NS - 2>();  // this thread's copies of stage st have landed
+    __syncthreads();          // everyone's; and stage st - 1 is consumed, its slot free
+    issue(st + NS - 1);
+    const double* sg = ring + (st % NS) * STAGE;
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) {
+      const int c = gq + j * GR;
+      const int64_t col = (int64_t)st * SC + c;
+      if (col < nb) {
+        md<M> u, xx;
+#pragma unroll
+        for (int k = 0; k < M; ++k) {
+          u.v[k] = sg[(k * SC + c) * RB + r];
+          xx.v[k] = xs[k * nb + col];
+        }
+        if (NACC == 2 && ((st * CPT + j) & 1)) acc1.add_prod(u, xx);  // warp-uniform
+        else acc0.add_prod(u, xx);
+      }
     }
   }
-#pragma unroll
-  for (int t = 0; t < RPT; ++t) part[g][lane + 32 * t] = acc[t];
+  cp_async_wait<0>();
+  acc0.merge(acc1);
+  part[gq][r] = acc0;
   __syncthreads();
-  // fixed-order tree over the G column groups (exact accumulator merges)
+  // fixed-order tree over the column groups (exact accumulator merges)
 #pragma unroll
-  for (int stride = G / 2; stride >= 1; stride >>= 1) {
-    if (g < stride) {
-#pragma unroll
-      for (int t = 0; t < RPT; ++t) {
-        Acc<M> a = part[g][lane + 32 * t];
-        a.merge(part[g + stride][lane + 32 * t]);
-        part[g][lane + 32 * t] = a;
-      }
+  for (int stride = GR / 2; stride >= 1; stride >>= 1) {
+    if (gq < stride) {
+      Acc<M> a = part[gq][r];
+      a.merge(part[gq + stride][r]);
+      part[gq][r] = a;
     }
     __syncthreads();
   }
-  for (int e = threadIdx.x; e < 32 * RPT; e += 32 * G) {
-    const int64_t rho = rbase + e;
-    if (rho >= row1) continue;
-    const md<M> t = part[0][e].get();
-    md<M> bb = ld<M>(b, psb, rho);
-    st<M>(b, psb, rho, add<M>(bb, neg(t)));
+  if (gq == 0 && rb + r < row1) {
+    const md<M> t = part[0][r].get();
+    const md<M> bb = ld<M>(b, psb, rb + r);
+    st<M>(b, psb, rb + r, add<M>(bb, neg(t)));
   }
 }
 
 // Us (nullable): nb x (ntiles nb) workspace for the row-scaled copy (the diagonal absorbed, see A7)
 template <int M>
-void launch_invert(cudaStream_t st, int64_t ntiles, int64_t nb, CMat U, Mat Vt, Mat Us, int* info) {
+// info_off: global row index of the first tile's first row (dev_info reports global 1-based rows)
+void launch_invert(cudaStream_t st, int64_t ntiles, int64_t nb, CMat U, Mat Vt, Mat Us, int* info, int64_t info_off) {
   const int threads = 256, nwarp = threads / 32;
   const int64_t ny = cdiv(nb, nwarp);
   dim3 grid((unsigned)ntiles, (unsigned)ny);
   const size_t smem = sizeof(double) * M * nb;
   if (Us.p) {
-    MDLS_LAUNCH(F_INVERT, st, scale_tiles_kernel<M><<<(unsigned)ntiles, threads, smem, st>>>(nb, U, Us, info));
+    const dim3 sgrid((unsigned)ntiles, (unsigned)std::max<int64_t>(1, std::min<int64_t>(8, nb / 16)));
+    MDLS_LAUNCH(F_INVERT, st, scale_tiles_kernel<M><<<sgrid, threads, smem, st>>>(nb, U, Us, info, info_off));
     const CMat C = cm(Us);
-    if (nb <= 32) MDLS_LAUNCH(F_INVERT, st, invert_tiles_kernel<M, 1, true><<<grid, threads, 0, st>>>(nb, U, C, Vt, info));
-    else if (nb <= 64) MDLS_LAUNCH(F_INVERT, st, invert_tiles_kernel<M, 2, true><<<grid, threads, 0, st>>>(nb, U, C, Vt, info));
-    else if (nb <= 128) MDLS_LAUNCH(F_INVERT, st, invert_tiles_kernel<M, 4, true><<<grid, threads, 0, st>>>(nb, U, C, Vt, info));
-    else MDLS_LAUNCH(F_INVERT, st, invert_tiles_kernel<M, 8, true><<<grid, threads, 0, st>>>(nb, U, C, Vt, info));
+    if (nb <= 32) MDLS_LAUNCH(F_INVERT, st, invert_tiles_kernel<M, 1, true><<<grid, threads, 0, st>>>(nb, U, C, Vt, info, info_off));
+    else if (nb <= 64) MDLS_LAUNCH(F_INVERT, st, invert_tiles_kernel<M, 2, true><<<grid, threads, 0, st>>>(nb, U, C, Vt, info, info_off));
+    else if (nb <= 128) MDLS_LAUNCH(F_INVERT, st, invert_tiles_kernel<M, 4, true><<<grid, threads, 0, st>>>(nb, U, C, Vt, info, info_off));
+    else MDLS_LAUNCH(F_INVERT, st, invert_tiles_kernel<M, 8, true><<<grid, threads, 0, st>>>(nb, U, C, Vt, info, info_off));
     return;
   }
   const CMat C{nullptr, 0, 0};
-  if (nb <= 32) MDLS_LAUNCH(F_INVERT, st, invert_tiles_kernel<M, 1, false><<<grid, threads, smem, st>>>(nb, U, C, Vt, info));
-  else if (nb <= 64) MDLS_LAUNCH(F_INVERT, st, invert_tiles_kernel<M, 2, false><<<grid, threads, smem, st>>>(nb, U, C, Vt, info));
-  else if (nb <= 128) MDLS_LAUNCH(F_INVERT, st, invert_tiles_kernel<M, 4, false><<<grid, threads, smem, st>>>(nb, U, C, Vt, info));
-  else MDLS_LAUNCH(F_INVERT, st, invert_tiles_kernel<M, 8, false><<<grid, threads, smem, st>>>(nb, U, C, Vt, info));
+  if (nb <= 32) MDLS_LAUNCH(F_INVERT, st, invert_tiles_kernel<M, 1, false><<<grid, threads, smem, st>>>(nb, U, C, Vt, info, info_off));
+  else if (nb <= 64) MDLS_LAUNCH(F_INVERT, st, invert_tiles_kernel<M, 2, false><<<grid, threads, smem, st>>>(nb, U, C, Vt, info, info_off));
+  else if (nb <= 128) MDLS_LAUNCH(F_INVERT, st, invert_tiles_kernel<M, 4, false><<<grid, threads, smem, st>>>(nb, U, C, Vt, info, info_off));
+  else MDLS_LAUNCH(F_INVERT, st, invert_tiles_kernel<M, 8, false><<<grid, threads, smem, st>>>(nb, U, C, Vt, info, info_off));
 }
 
 template <int M>
 void launch_bs_mulinv(cudaStream_t st, int64_t nb, int64_t tile, CMat Vt, const double* b, int64_t psb, double* x,
                       int64_t psx) {
-  MDLS_LAUNCH(F_BS, st, bs_mulinv_kernel<M><<<(unsigned)cdiv(nb, 8), 256, 0, st>>>(nb, tile, Vt, b, psb, x, psx));
+  const dim3 grid((unsigned)cdiv(nb, 8));
+  if (nb <= 64) MDLS_LAUNCH(F_BS, st, launch_pdl(bs_mulinv_kernel<M, 2>, grid, dim3(256), 0, st, nb, tile, Vt, b, psb, x, psx));
+  else if (nb <= 128) MDLS_LAUNCH(F_BS, st, launch_pdl(bs_mulinv_kernel<M, 4>, grid, dim3(256), 0, st, nb, tile, Vt, b, psb, x, psx));
+  else MDLS_LAUNCH(F_BS, st, launch_pdl(bs_mulinv_kernel<M, 8>, grid, dim3(256), 0, st, nb, tile, Vt, b, psb, x, psx));
 }
 
-// rows [row0, row1): CTA = 32 rows x GC column groups (1024 / 512 threads), so
-// even the short late steps spread over many SMs; `critical` (one tile of rows on the
-// back substitution's chain): twice the column groups, half the sequential products
+// rows [row0, row1): RB = 32 rows per CTA when that still gives two CTAs per SM, else RB = 8;
+// NS stages of 16 KB (dynamic shared memory beyond 48 KB: attribute set once per device)
+template <int M, int RB, int NS, int MINB, int NACC>
+void bs_update_launch(cudaStream_t st, int64_t nb, int64_t tile, int64_t row0, int64_t row1, CMat U, const double* x,
+                      int64_t psx, double* b, int64_t psb) {
+  static bool attr_set[kMaxDev];
+  const int dev = cur_dev();
+  const size_t smem = sizeof(double) * ((size_t)M * nb + (size_t)NS * 2048);
+  if (!attr_set[dev]) {
+    cudaFuncSetAttribute(bs_update_kernel<M, RB, NS, MINB, NACC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(sizeof(double) * ((size_t)M * 256 + (size_t)NS * 2048)));
+    attr_set[dev] = true;
+  }
+  MDLS_LAUNCH(F_BS, st, launch_pdl(bs_update_kernel<M, RB, NS, MINB, NACC>, dim3((unsigned)cdiv(row1 - row0, RB)),
+                                    dim3(256), smem, st, nb, tile, row0, row1, U, x, psx, b, psb));
+}
+// variant (MDLS_BSU): 0 = NS 4, two CTAs per SM, two accumulator chains per thread (default, measured
+// 4.44 ms at config 4); 1 = the same with one chain (4.52 ms); 2 = NS 3, three CTAs per SM, two chains (5.17)
+
+template <int M, int RB>
+void bs_update_variant(cudaStream_t st, int64_t nb, int64_t tile, int64_t row0, int64_t row1, CMat U, const double* x,
+                       int64_t psx, double* b, int64_t psb) {
+  static const int v = [] {
+    const char* e = getenv("MDLS_BSU");
+    return e ? atoi(e) : 0;
+  }();
+  if (v == 1) bs_update_launch<M, RB, 4, 2, 1>(st, nb, tile, row0, row1, U, x, psx, b, psb);
+  else if (v == 2) bs_update_launch<M, RB, 3, 3, 2>(st, nb, tile, row0, row1, U, x, psx, b, psb);
+  else bs_update_launch<M, RB, 4, 2, 2>(st, nb, tile, row0, row1, U, x, psx, b, psb);
+}
 template <int M>
 void launch_bs_update(cudaStream_t st, int64_t nb, int64_t tile, int64_t row0, int64_t row1, CMat U, const double* x,
                       int64_t psx, double* b, int64_t psb) {
   const int64_t rows = row1 - row0;
   if (rows <= 0) return;
-  constexpr int GC = (M == 2) ? 32 : 16;  // column groups (registers / smem bound)
-  MDLS_LAUNCH(F_BS, st, bs_update_kernel<M, GC, 1><<<(unsigned)cdiv(rows, 32), 32 * GC, 0, st>>>(nb, tile, row0, row1, U, x, psx, b, psb));
+  if (cdiv(rows, 32) >= 2 * num_sms()) bs_update_variant<M, 32>(st, nb, tile, row0, row1, U, x, psx, b, psb);
+  else bs_update_variant<M, 8>(st, nb, tile, row0, row1, U, x, psx, b, psb);
 }
 
 #define MDLS_INSTANTIATE_BS(MM)                                                                                \
-  template void launch_invert<MM>(cudaStream_t, int64_t, int64_t, CMat, Mat, Mat, int*);                                     \
+  template void launch_invert<MM>(cudaStream_t, int64_t, int64_t, CMat, Mat, Mat, int*, int64_t);                                     \
   template void launch_bs_mulinv<MM>(cudaStream_t, int64_t, int64_t, CMat, const double*, int64_t, double*,    \
                                      int64_t);                                                                 \
   template void launch_bs_update<MM>(cudaStream_t, int64_t, int64_t, int64_t, int64_t, CMat, const double*,  \

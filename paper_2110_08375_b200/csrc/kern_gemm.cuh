@@ -26,16 +26,6 @@ __device__ __forceinline__ md<M> apply_mode(int mode, const md<M>& c, const md<M
   }
 }
 
-// asynchronous global -> shared copies (LDGSTS): 8-byte granules, so any double-aligned operand
-// (sub-matrix views with odd row offsets or odd leading dimensions included) can be staged; a
-// false predicate copies nothing and zero-fills the destination
-__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool pred) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s), "l"(gmem), "r"(pred ? 8 : 0) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 // pipeline depth and padded shared-memory rows per precision (dynamic shared memory)
 template <int M, int V, bool TA, bool TB>

@@ -467,13 +467,23 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
       " @!p bra MDLS_WAIT_%=;\n}\n" :: "r"(bar), "r"(parity) : "memory");
 }
-// push an md-like value of NV doubles (NV even) to the same smem slot of CTA `rank`
+__device__ __forceinline__ void st_async_f64(uint32_t raddr, double x, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];"
+               :: "r"(raddr), "d"(x), "r"(rbar) : "memory");
+}
+// push an md-like value of NV doubles to the same smem slot of CTA `rank` (pairs as v2 stores; NV = 1,
+// plain double, as one 8-byte store)
 template <int NV>
 __device__ __forceinline__ void push_vals(const double* v, const void* local_slot, int rank, uint32_t local_bar) {
   const uint32_t ra = cluster_addr(smem_addr(local_slot), rank);
   const uint32_t rb = cluster_addr(local_bar, rank);
+  if constexpr (NV % 2 == 1) {
+    static_assert(NV == 1, "odd md widths other than plain double");
+    st_async_f64(ra, v[0], rb);
+  } else {
 #pragma unroll
-  for (int k = 0; k < NV; k += 2) st_async_v2(ra + 8 * k, v[k], v[k + 1], rb);
+    for (int k = 0; k < NV; k += 2) st_async_v2(ra + 8 * k, v[k], v[k + 1], rb);
+  }
 }
 
 // t - v w through the level-bin accumulator (one normalisation)
@@ -794,7 +804,6 @@ __device__ __forceinline__ void leaf_body(const LeafArgs<M>& a, bool init_bars, 
   constexpr int GS = 16;  // lanes per column in the final partial sum
   static_assert(V >= 1 && B % TPR == 0 && 32 % TPR == 0, "leaf shape");
   static_assert(B * NW <= NT && 32 % NW == 0 && NW >= 4 && B * GS <= NT && (B * NW) % 32 == 0, "leaf threads");
-  static_assert(M % 2 == 0, "pushes move pairs of doubles");
 
   cg::cluster_group cluster = cg::this_cluster();
   const int C = (int)cluster.num_blocks();
@@ -836,6 +845,10 @@ __device__ __forceinline__ void leaf_body(const LeafArgs<M>& a, bool init_bars, 
 #pragma unroll
     for (int k = 0; k < M; ++k) t[q].v[k] = valid ? __ldcg(a.A.p + k * a.A.ps + (a.js + c) * a.A.ld + gi) : 0.0;
   }
+  // PDL (leaf_reg_launch): the leaf's own columns are final before the previous leaf ends (they are written only
+  // by the near-window updates, a full event dependency), so they load above; the previous leaf's Y, T (prologue)
+  // only after its grid has completed
+  pdl_wait();
   if (a.jsp >= 0) leaf_prologue<M, B, TPR, NT>(a, cluster, C, rank, t, Rp, valid, gi, row0, zinit, zpar);
   else cluster.sync();  // every CTA's barriers initialised and armed before the first push
 
@@ -921,7 +934,32 @@ __device__ __forceinline__ void leaf_body(const LeafArgs<M>& a, bool init_bars, 
     const md<M> sigma = G[l], x1 = piv[buf][l];
     const bool deg = sigma.v[0] == 0.0;
     const bool pos = x1.v[0] > 0.0;
-    if constexpr (M == 2) {
+    if constexpr (M == 1) {
+      // plain double: the same chain as double double, one rounded operation per step
+      if (warp == 0) {
+        const double x = x1.v[0], sg = sigma.v[0];
+        double mu = x, beta = 0.0, rv1 = 1.0;
+        if (!deg) {
+          mu = __dsqrt_rn(__dadd_rn(__dmul_rn(x, x), sg));
+          const double sv = pos ? __dadd_rn(x, mu) : __dsub_rn(x, mu);
+          const double rmu = __drcp_rn(mu);
+          rv1 = pos ? -__ddiv_rn(sv, sg) : __drcp_rn(sv);                           // 1/v1
+          beta = pos ? __dmul_rn(__ddiv_rn(sg, sv), rmu) : -__dmul_rn(sv, rmu);    // 2 v1^2 / (sigma + v1^2)
+        }
+        if (lane < B) {
+          const int c = lane;
+          const double pc = piv[buf][c].v[0];
+          const double u = deg ? pc : __fma_rn(rv1, G[c].v[0], pc);
+          if (c < l) SY[c][l] = md<1>{{u}};
+          W[c] = md<1>{{(c > l && !deg) ? __dmul_rn(beta, u) : 0.0}};
+        }
+        if (lane == 0) {
+          sc_mu = md<1>{{mu}};
+          sc_rv1 = md<1>{{rv1}};
+          betas[l] = md<1>{{beta}};
+        }
+      }
+    } else if constexpr (M == 2) {
       // double double: warp 0 computes the three independent chains inline (ILP), no extra barrier
       if (warp == 0) {
         md<2> mu = x1, beta = md_zero<2>(), rv1 = md_from<2>(1.0);
@@ -981,7 +1019,7 @@ __device__ __forceinline__ void leaf_body(const LeafArgs<M>& a, bool init_bars, 
     }  // this CTA's rows of T(:, l-1)
     __syncthreads();
     LEAF_MARK(l, 5);
-    if constexpr (M != 2) {
+    if constexpr (M > 2) {
       static_assert(NT >= 32 * B, "one warp per leaf column");
       // phase B: warp 0 forms rs = 1/s (the long reciprocal); warps 1..B-1 meanwhile, in two steps (named
       // barrier 1): x1 > 0: rv1 = 1/v1 = -s/sigma (warp 1), bq = sigma/mu (warp 2), then per column c != l
@@ -1079,6 +1117,7 @@ __device__ __forceinline__ void leaf_body(const LeafArgs<M>& a, bool init_bars, 
   }
 
   // ---- last T column, write-back of R/v, explicit Y, beta, T ----
+  pdl_trigger();  // only the write-back remains: the next leaf's cluster may launch now
   __syncthreads();
   if (warp == 3) {
     if constexpr (M == 8) leaf_t_column_warp<M>(Ts, SY, betas, B - 1, rank, C, lane);
@@ -1112,7 +1151,7 @@ __global__ void __launch_bounds__(NT) leaf_reg_kernel(LeafArgs<M> a) {
 }
 
 template <int M, int B, int TPR, int NT>
-cudaError_t leaf_reg_launch(cudaStream_t st, const LeafArgs<M>& la, int C) {
+cudaError_t leaf_reg_launch(cudaStream_t st, const LeafArgs<M>& la, int C, bool pdl = false) {
   auto kern = leaf_reg_kernel<M, B, TPR, NT>;
   // Exclusive SMs: request enough shared memory that no other CTA (the concurrent trailing / Q
   // GEMMs of the other streams) can share the leaf's SMs and their FP64 pipes -- the leaf is a
@@ -1140,13 +1179,15 @@ cudaError_t leaf_reg_launch(cudaStream_t st, const LeafArgs<M>& la, int C) {
   cfg.blockDim = dim3(NT, 1, 1);
   cfg.dynamicSmemBytes = dyn;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = C;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // overlap the launch with the previous leaf's tail
+  attr[1].val.programmaticStreamSerializationAllowed = (pdl && pdl_enabled()) ? 1 : 0;  // chain only
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   trace_begin(st, F_PANEL);
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, la);
   trace_end(st, F_PANEL);
@@ -1206,7 +1247,7 @@ cudaError_t launch_leaf(cudaStream_t st, int64_t Mrows, int64_t js, int64_t bmax
   const int64_t rows = Mrows - js;
   const size_t cap = 200 * 1024;
   int B = 1;
-  while (B * 2 <= bmax && B * 2 <= (M == 2 ? 16 : 8)) B *= 2;  // B = 32 measured slower per column
+  while (B * 2 <= bmax && B * 2 <= (M <= 2 ? 16 : 8)) B *= 2;  // B = 32 measured slower per column
   for (;;) {
     const int C = (int)std::max<int64_t>(1, std::min<int64_t>(csize, rows));
     const int64_t R = cdiv(rows, C);
@@ -1219,25 +1260,25 @@ cudaError_t launch_leaf(cudaStream_t st, int64_t Mrows, int64_t js, int64_t bmax
       return v && v[0] == 's';
     }();
     if (!force_smem && B >= 4 && R <= 64) {
-      if constexpr (M == 2) e = (B == 16) ? leaf_reg_launch<M, 16, 4, 256>(st, la, C)
+      if constexpr (M <= 2) e = (B == 16) ? leaf_reg_launch<M, 16, 4, 256>(st, la, C)
                                           : (B == 8 ? leaf_reg_launch<M, 8, 4, 256>(st, la, C)
                                                     : leaf_reg_launch<M, 4, 4, 256>(st, la, C));
       else e = (B == 8) ? leaf_reg_launch<M, 8, 4, 256>(st, la, C) : leaf_reg_launch<M, 4, 4, 256>(st, la, C);
     } else if (!force_smem && M <= 4 && B >= 4 && R <= 128) {
-      if constexpr (M == 2) e = (B == 16) ? leaf_reg_launch<M, 16, 4, 512>(st, la, C)
+      if constexpr (M <= 2) e = (B == 16) ? leaf_reg_launch<M, 16, 4, 512>(st, la, C)
                                           : (B == 8 ? leaf_reg_launch<M, 8, 4, 512>(st, la, C)
                                                     : leaf_reg_launch<M, 4, 4, 512>(st, la, C));
       else e = (B == 8) ? leaf_reg_launch<M, 8, 4, 512>(st, la, C) : leaf_reg_launch<M, 4, 4, 512>(st, la, C);
     } else {
     switch (B) {
       case 32:
-        if constexpr (M == 2) {
+        if constexpr (M <= 2) {
           e = leaf_launch_impl<M, 32, 4>(st, la, C);
           break;
         }
         [[fallthrough]];
       case 16:
-        if constexpr (M == 2) {
+        if constexpr (M <= 2) {
           e = leaf_launch_impl<M, 16, 4>(st, la, C);
           break;
         }
@@ -1270,14 +1311,14 @@ cudaError_t launch_leaf_chain(cudaStream_t st, int64_t Mrows, int64_t js, int B,
   const int C = (int)std::max<int64_t>(1, std::min<int64_t>(leaf_cluster_size(), rows));
   const int64_t R = cdiv(rows, C);
   LeafArgs<M> la{Mrows, js, R, A, Y, beta, bps, T, info, Y, Tp, jsp};
-  if constexpr (M == 2) {
-    if (R <= 64) return B == 16 ? leaf_reg_launch<M, 16, 4, 256>(st, la, C) : leaf_reg_launch<M, 8, 4, 256>(st, la, C);
-    return B == 16 ? leaf_reg_launch<M, 16, 4, 512>(st, la, C) : leaf_reg_launch<M, 8, 4, 512>(st, la, C);
+  if constexpr (M <= 2) {
+    if (R <= 64) return B == 16 ? leaf_reg_launch<M, 16, 4, 256>(st, la, C, true) : leaf_reg_launch<M, 8, 4, 256>(st, la, C, true);
+    return B == 16 ? leaf_reg_launch<M, 16, 4, 512>(st, la, C, true) : leaf_reg_launch<M, 8, 4, 512>(st, la, C, true);
   } else if constexpr (M == 4) {
-    if (R <= 64) return leaf_reg_launch<M, 8, 4, 256>(st, la, C);
-    return leaf_reg_launch<M, 8, 4, 512>(st, la, C);
+    if (R <= 64) return leaf_reg_launch<M, 8, 4, 256>(st, la, C, true);
+    return leaf_reg_launch<M, 8, 4, 512>(st, la, C, true);
   } else {
-    return leaf_reg_launch<M, 8, 4, 256>(st, la, C);
+    return leaf_reg_launch<M, 8, 4, 256>(st, la, C, true);
   }
 }
 

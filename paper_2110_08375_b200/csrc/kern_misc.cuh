@@ -37,7 +37,7 @@ __global__ void md_op_warp_kernel(int op, int64_t n, const double* __restrict__ 
     const md<M> x = ld<M>(a, ps, e);
     const md<M> y = (op == 7) ? ld<M>(b, ps, e) : md_zero<M>();
     md<M> r;
-    if constexpr (M == 2) {
+    if constexpr (M <= 2) {
       r = (op == 7) ? mul<M>(x, y) : (op == 8 ? sqrt_fast<M>(x) : recip_fast<M>(x));
     } else {
       r = (op == 7) ? wmul<M>(x, y) : (op == 8 ? w_sqrt_fast<M>(x) : w_recip_fast<M>(x));

@@ -31,7 +31,7 @@ inline int leaf_cluster_size() {
 template <int M>
 inline int chain_leaf_width(int64_t Mrows, int64_t js, int64_t bmax) {
   int B = 1;
-  while (B * 2 <= bmax && B * 2 <= (M == 2 ? 16 : 8)) B *= 2;
+  while (B * 2 <= bmax && B * 2 <= (M <= 2 ? 16 : 8)) B *= 2;
   if (B < 8) return 0;
   const int64_t rows = Mrows - js;
   const int C = (int)std::max<int64_t>(1, std::min<int64_t>(leaf_cluster_size(), rows));
@@ -45,7 +45,7 @@ cudaError_t launch_leaf_chain(cudaStream_t st, int64_t Mrows, int64_t js, int B,
                               int64_t bps, Mat T, int* info, Mat Tp, int64_t jsp);
 
 template <int M>
-void launch_invert(cudaStream_t st, int64_t ntiles, int64_t nb, CMat U, Mat Vt, Mat Us, int* info);
+void launch_invert(cudaStream_t st, int64_t ntiles, int64_t nb, CMat U, Mat Vt, Mat Us, int* info, int64_t info_off);
 
 template <int M>
 void launch_bs_mulinv(cudaStream_t st, int64_t nb, int64_t tile, CMat Vt, const double* b, int64_t psb, double* x,

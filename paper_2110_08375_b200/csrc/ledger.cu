@@ -144,10 +144,12 @@ int max_cluster_size() {
 namespace {
 
 struct T1 {
-  double add, mul, div;
+  double add, mul, div, sqrt;
 };
-// Table 1 sums
-constexpr T1 kT1[3] = {{20, 23, 70}, {89, 336, 893}, {269, 1742, 5126}};
+// Table 1 sums; an md sqrt is priced as 1 div + 2 mul (Z12).
+// Index 3 is plain double (1d): every operation is one double flop.
+constexpr T1 kT1[4] = {{20, 23, 70, 70 + 2 * 23}, {89, 336, 893, 893 + 2 * 336}, {269, 1742, 5126, 5126 + 2 * 1742},
+                       {1, 1, 1, 1}};
 
 void count_house(int64_t n_j, mdls_counts* c) {
   // sigma: n-1 squares and sums; x1^2 + sigma; v1; beta = 2 v1^2 / (sigma + v1^2);
@@ -245,7 +247,7 @@ int count(int pidx, int op, int64_t M, int64_t K, int64_t nb, mdls_counts* out) 
   out->total_flops = 0;
   for (int s = 0; s < MDLS_NSTAGES; ++s) {
     out->flops[s] = out->add[s] * t.add + out->mul[s] * t.mul + out->div[s] * t.div +
-                    out->sqrt[s] * (t.div + 2 * t.mul);
+                    out->sqrt[s] * t.sqrt;
     out->total_flops += out->flops[s];
   }
   return 0;
@@ -354,10 +356,13 @@ int mdls_trace_collect(double* stage_ms, double* family_ms, int64_t* family_laun
   return rc ? MDLS_ERR_CUDA : (int)recs.size();
 }
 
-int mdls_limbs(int prec_index) { return prec_index == 0 ? 2 : prec_index == 1 ? 4 : prec_index == 2 ? 8 : -1; }
+int mdls_limbs(int prec_index) {
+  return prec_index == 0 ? 2 : prec_index == 1 ? 4 : prec_index == 2 ? 8 : prec_index == 3 ? 1 : -1;
+}
 
 int mdls_count_dd(int op, int64_t M, int64_t K, int64_t nb, mdls_counts* out) { return count(0, op, M, K, nb, out); }
 int mdls_count_qd(int op, int64_t M, int64_t K, int64_t nb, mdls_counts* out) { return count(1, op, M, K, nb, out); }
 int mdls_count_od(int op, int64_t M, int64_t K, int64_t nb, mdls_counts* out) { return count(2, op, M, K, nb, out); }
+int mdls_count_d(int op, int64_t M, int64_t K, int64_t nb, mdls_counts* out) { return count(3, op, M, K, nb, out); }
 
 }  // extern "C"

@@ -300,9 +300,12 @@ __device__ __noinline__ md<M> gen_sqrt(const md<M>& a) {
 // ----------------------------------------------------------------------------
 // precision dispatch
 // ----------------------------------------------------------------------------
+// M = 1 is plain IEEE double ("1d": the paper's double precision reference rows):
+// one correctly rounded operation each, no error-free transformation.
 template <int M>
 __device__ __forceinline__ md<M> add(const md<M>& a, const md<M>& b) {
-  if constexpr (M == 2) return dd_add(a, b);
+  if constexpr (M == 1) return md<1>{{__dadd_rn(a.v[0], b.v[0])}};
+  else if constexpr (M == 2) return dd_add(a, b);
   else return gen_add<M>(a, b);
 }
 template <int M>
@@ -311,22 +314,26 @@ __device__ __forceinline__ md<M> sub(const md<M>& a, const md<M>& b) {
 }
 template <int M>
 __device__ __forceinline__ md<M> mul(const md<M>& a, const md<M>& b) {
-  if constexpr (M == 2) return dd_mul(a, b);
+  if constexpr (M == 1) return md<1>{{__dmul_rn(a.v[0], b.v[0])}};
+  else if constexpr (M == 2) return dd_mul(a, b);
   else return gen_mul<M>(a, b);
 }
 template <int M>
 __device__ __forceinline__ md<M> mul_d(const md<M>& a, double b) {
-  if constexpr (M == 2) return dd_mul_d(a, b);
+  if constexpr (M == 1) return md<1>{{__dmul_rn(a.v[0], b)}};
+  else if constexpr (M == 2) return dd_mul_d(a, b);
   else return gen_mul_d<M>(a, b);
 }
 template <int M>
 __device__ __forceinline__ md<M> div(const md<M>& a, const md<M>& b) {
-  if constexpr (M == 2) return dd_div(a, b);
+  if constexpr (M == 1) return md<1>{{__ddiv_rn(a.v[0], b.v[0])}};
+  else if constexpr (M == 2) return dd_div(a, b);
   else return gen_div<M>(a, b);
 }
 template <int M>
 __device__ __forceinline__ md<M> sqrt(const md<M>& a) {
-  if constexpr (M == 2) return dd_sqrt(a);
+  if constexpr (M == 1) return md<1>{{__dsqrt_rn(a.v[0])}};
+  else if constexpr (M == 2) return dd_sqrt(a);
   else return gen_sqrt<M>(a);
 }
 // acc + a*b  (md mul, then md add: one "pair")
@@ -389,7 +396,9 @@ __device__ __forceinline__ md<H> rsqrt_to(const md<M>& a) {
 template <int M>
 __device__ __noinline__ md<M> sqrt_fast(const md<M>& a) {
   if (a.v[0] == 0.0) return md_zero<M>();
-  if constexpr (M == 2) {
+  if constexpr (M == 1) {
+    return md<1>{{__dsqrt_rn(a.v[0])}};
+  } else if constexpr (M == 2) {
     // Karp: sqrt(a) = a x + x (a - (a x)^2) / 2 with x = rsqrt(a0) (hardware-seeded double);
     // a0 - p is exact (Sterbenz), so the residual needs three plain operations
     const double x = ::rsqrt(a.v[0]);
@@ -417,7 +426,9 @@ __device__ __forceinline__ md<P> recip_step(const md<P>& d, const md<P>& y) {
 }
 template <int M>
 __device__ __noinline__ md<M> recip_fast(const md<M>& d) {
-  if constexpr (M == 2) {
+  if constexpr (M == 1) {
+    return md<1>{{__drcp_rn(d.v[0])}};
+  } else if constexpr (M == 2) {
     const double y0 = __drcp_rn(d.v[0]);
     const md<2> e = dd_add(md_from<2>(1.0), neg(dd_mul_d(d, y0)));  // 1 - d y0, tiny
     md<2> r;

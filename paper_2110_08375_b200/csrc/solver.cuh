@@ -488,9 +488,13 @@ void backsub(cudaStream_t st, int64_t n, int64_t nb, CMat U, const double* y, in
   }();
   const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(N, chunk_env > 0 ? chunk_env : N));
   std::vector<cudaEvent_t> inv_ready((size_t)N, nullptr);
-  for (int64_t hi = N; hi > 0; hi -= chunk) {
-    const int64_t lo = std::max<int64_t>(0, hi - chunk);
-    launch_invert<M>(sinv, hi - lo, nb, sub(U, lo * nb, lo * nb), sub(Vt, 0, lo * nb), sub(Us, 0, lo * nb), info_slot);
+  // bottom-first chunks growing 2, 4, 8, ... up to `chunk` tiles: the chain's first step waits only for a
+  // two-tile inversion, later chunks finish ahead of the chain
+  int64_t step = std::min<int64_t>(chunk, 2);
+  for (int64_t hi = N; hi > 0; hi -= step, step = std::min<int64_t>(chunk, 2 * step)) {
+    const int64_t lo = std::max<int64_t>(0, hi - step);
+    launch_invert<M>(sinv, hi - lo, nb, sub(U, lo * nb, lo * nb), sub(Vt, 0, lo * nb), sub(Us, 0, lo * nb), info_slot,
+                     lo * nb);
     cudaEvent_t ev = pool_event();
     cudaEventRecord(ev, sinv);
     for (int64_t t = lo; t < hi; ++t) inv_ready[(size_t)t] = ev;

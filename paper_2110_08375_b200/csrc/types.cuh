@@ -54,6 +54,35 @@ struct PlanImpl {
 cudaStream_t capture_begin();
 int capture_end(cudaStream_t cs, int64_t launches, void** plan_out);
 cudaEvent_t pool_event();
+// Programmatic dependent launch (PDL): a kernel launched with launch_pdl may start while its
+// stream predecessor still runs; it calls pdl_trigger() early (lets ITS successor launch) and
+// pdl_wait() before touching anything the predecessor writes (griddepcontrol.wait returns once
+// the predecessor grid has completed and its memory is visible; a no-op without the attribute).
+// Work that reads only inputs nobody in flight writes (e.g. U in the back substitution) goes
+// before the wait, overlapping the predecessor's tail and the launch latency.  MDLS_PDL=0: off.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("MDLS_PDL");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
 #define MDLS_LAUNCH(FAM, ST, ...)          \
   do {                                     \
     ::mdls::trace_begin((ST), (FAM));      \
@@ -96,6 +125,18 @@ inline int num_sms() {
 int max_cluster_size();
 
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// asynchronous global -> shared copies (LDGSTS): 8-byte granules, so any double-aligned operand
+// (sub-matrix views with odd row offsets or odd leading dimensions included) can be staged; a
+// false predicate copies nothing and zero-fills the destination
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool pred) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s), "l"(gmem), "r"(pred ? 8 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 inline int grid_for(int64_t n, int threads) {
@@ -117,6 +158,11 @@ struct Tile {
 };
 template <int M, int V>
 struct GemmTile;
+// plain double (1d): the dd shapes (one FMA per pair instead of 12 FP64 operations)
+template <> struct GemmTile<1, 0> : Tile<64, 64, 16, 4, 4> {};
+template <> struct GemmTile<1, 1> : Tile<32, 32, 16, 2, 2> {};
+template <> struct GemmTile<1, 2> : Tile<16, 64, 16, 1, 4> {};
+template <> struct GemmTile<1, 3> : Tile<64, 16, 16, 4, 1> {};
 template <> struct GemmTile<2, 0> : Tile<64, 64, 16, 4, 4> {};
 template <> struct GemmTile<2, 1> : Tile<32, 32, 16, 2, 2> {};
 template <> struct GemmTile<2, 2> : Tile<16, 64, 16, 1, 4> {};

@@ -26,7 +26,7 @@ from __future__ import annotations
 
 import numpy as np
 
-PRECISIONS = {"dd": 2, "qd": 4, "od": 8}
+PRECISIONS = {"d": 1, "dd": 2, "qd": 4, "od": 8}
 
 
 def limbs(prec) -> int:

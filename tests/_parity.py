@@ -4,14 +4,14 @@ Tolerance (north_star): componentwise, scaled by the
 column (or vector) max norm of the oracle result:
     |R_gpu - R_orc|_ij <= 1e3 * n * u * max_i |R_orc(i, j)|
     |x_gpu - x_orc|_i  <= 1e3 * n * u * max_i |x_orc(i)|
-with u = 2^-104 (dd), 2^-208 (qd), 2^-416 (od) and n the number of columns.
+with u = 2^-53 (d, plain double), 2^-104 (dd), 2^-208 (qd), 2^-416 (od) and n the number of columns.
 Differences are taken in md arithmetic (oracle md sub), leading limb.
 """
 from __future__ import annotations
 
 import numpy as np
 
-U_OF = {"dd": 2.0 ** -104, "qd": 2.0 ** -208, "od": 2.0 ** -416}
+U_OF = {"d": 2.0 ** -53, "dd": 2.0 ** -104, "qd": 2.0 ** -208, "od": 2.0 ** -416}
 
 
 def md_diff(orc, prec, a: np.ndarray, b: np.ndarray) -> np.ndarray:

@@ -19,7 +19,7 @@ def declared_symbols():
     names = set(re.findall(r"\b(mdls_[a-z0-9_]+)\s*\(", src.split("#define MDLS_DECLARE")[0]))
     block = src.split("#define MDLS_DECLARE(P)")[1].split("MDLS_DECLARE(dd)")[0]
     stems = set(re.findall(r"\b(mdls_[a-z0-9_]+_)##P\s*\(", block))
-    for p in ("dd", "qd", "od"):
+    for p in re.findall(r"^MDLS_DECLARE\((\w+)\)", src, re.M):
         names |= {s + p for s in stems}
     return names
 
@@ -40,7 +40,7 @@ def test_version_limbs_strerror():
     assert b"invalid" in lib.mdls_strerror(-3)
 
 
-@pytest.mark.parametrize("prec", ["dd", "qd", "od"])
+@pytest.mark.parametrize("prec", ["d", "dd", "qd", "od"])
 def test_host_argument_checks(prec):
     """Invalid sizes are rejected with -i before any CUDA call (works without a GPU)."""
     qr = _lib.fn("mdls_qr_", prec)
@@ -60,7 +60,7 @@ def test_host_argument_checks(prec):
     assert op(0, 10, fake, nul, fake, 10, nul) == -4
     assert op(7, 10, fake, nul, fake, 10, nul) == -4                                       # warp mul needs b
     bat = _lib.fn("mdls_lstsq_batched_", prec)
-    m = {"dd": 2, "qd": 4, "od": 8}[prec]
+    m = {"d": 1, "dd": 2, "qd": 4, "od": 8}[prec]
     args = [4, 64, 64, 8, fake, 64, 4096, m * 4096, fake, 64, m * 64, fake, 64, m * 64, 1, 2, fake, 1 << 40, nul, nul]
     for i, v, rc in ((0, -1, -1), (3, 7, -4), (7, 100, -8), (10, 10, -11), (13, 1, -14), (15, 0, -16), (15, 17, -16),
                      (17, 10, -18)):
@@ -87,7 +87,7 @@ def _pairs(c, stage):
     return c["stages"][stage]["mul"]
 
 
-@pytest.mark.parametrize("prec", ["dd", "qd", "od"])
+@pytest.mark.parametrize("prec", ["d", "dd", "qd", "od"])
 def test_ledger_closed_forms(prec):
     M, K = 96, 64
     # nb = 1: every reflector is its own panel, the in-panel work vanishes and the
@@ -113,13 +113,14 @@ def test_ledger_closed_forms(prec):
     assert b["stages"]["invert"]["div"] == N * nb
 
 
-@pytest.mark.parametrize("prec", ["dd", "qd", "od"])
+@pytest.mark.parametrize("prec", ["d", "dd", "qd", "od"])
 def test_ledger_table1_weighting(prec):
     add, mul, div = mdls.T1_SUMS[prec]
     c = mdls.counts(prec, 2, 256, 256, 64)
     tot = 0.0
     for s, v in c["stages"].items():
-        f = v["add"] * add + v["mul"] * mul + v["div"] * div + v["sqrt"] * (div + 2 * mul)
+        sq = 1 if prec == "d" else div + 2 * mul  # md sqrt priced as 1 div + 2 mul (Z12); a double sqrt is 1 flop
+        f = v["add"] * add + v["mul"] * mul + v["div"] * div + v["sqrt"] * sq
         assert f == pytest.approx(v["flops"], rel=1e-15)
         tot += f
     assert tot == pytest.approx(c["total_flops"], rel=1e-15)

@@ -36,10 +36,10 @@ def _operands(prec, n, seed):
     return a, b
 
 
-@pytest.mark.parametrize("prec", ["dd", "qd", "od"])
+@pytest.mark.parametrize("prec", ["d", "dd", "qd", "od"])
 @pytest.mark.parametrize("op", ["add", "sub", "mul", "div", "sqrt"])
 def test_md_ops_bitwise(orc, mdls, dev, prec, op):
-    n = {"dd": 200_000, "qd": 50_000, "od": 10_000}[prec]
+    n = {"d": 200_000, "dd": 200_000, "qd": 50_000, "od": 10_000}[prec]
     a, b = _operands(prec, n, 17)
     if op == "sqrt":
         a = np.where(a[0] < 0, -a, a)

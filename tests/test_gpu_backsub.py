@@ -11,7 +11,7 @@ from ._parity import U_OF, md_diff, vec_ok
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("prec", ["dd", "qd", "od"])
+@pytest.mark.parametrize("prec", ["d", "dd", "qd", "od"])
 @pytest.mark.parametrize("n,nb", [(32, 32), (96, 32), (256, 64), (384, 128)])
 def test_invert_tiles_vs_oracle(orc, mdls, dev, prec, n, nb):
     U = inputs.lu_upper(n, prec, seed=n + nb)
@@ -31,7 +31,7 @@ def test_invert_tiles_vs_oracle(orc, mdls, dev, prec, n, nb):
             assert err <= tol, (t, c, err, tol)
 
 
-@pytest.mark.parametrize("prec", ["dd", "qd", "od"])
+@pytest.mark.parametrize("prec", ["d", "dd", "qd", "od"])
 @pytest.mark.parametrize("n,nb", [(8, 8), (64, 8), (96, 32), (640, 128)])
 def test_backsub_vs_oracle(orc, mdls, dev, prec, n, nb):
     U = inputs.lu_upper(n, prec, seed=7 * n + nb)

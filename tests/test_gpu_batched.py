@@ -21,7 +21,7 @@ def _stack(M, K, prec, seeds, dev):
     return probs, A, b
 
 
-@pytest.mark.parametrize("prec", ["dd", "qd", "od"])
+@pytest.mark.parametrize("prec", ["d", "dd", "qd", "od"])
 @pytest.mark.parametrize("M,K,nb,B,groups", [(96, 64, 16, 6, 3), (130, 128, 32, 5, 2), (64, 64, 8, 3, 4)])
 def test_batched_equals_single(orc, mdls, dev, prec, M, K, nb, B, groups):
     probs, A, b = _stack(M, K, prec, range(100, 100 + B), dev)

@@ -26,11 +26,11 @@ def _op(X, trans):
     return np.transpose(Xr, (0, 2, 1)) if trans else Xr
 
 
-@pytest.mark.parametrize("prec", ["dd", "qd", "od"])
+@pytest.mark.parametrize("prec", ["d", "dd", "qd", "od"])
 @pytest.mark.parametrize("m,n,k,ta,tb,mode", [(37, 29, 61, 0, 0, 0), (16, 70, 2000, 1, 0, 1), (130, 3, 513, 0, 1, 2),
                                               (9, 11, 7, 1, 1, 3), (64, 64, 128, 0, 0, 1)])
 def test_gemm_vs_oracle_dots(orc, mdls, dev, prec, m, n, k, ta, tb, mode):
-    ml = {"dd": 2, "qd": 4, "od": 8}[prec]
+    ml = inputs.limbs(prec)
     A = inputs.random_matrix(k if ta else m, m if ta else k, prec, seed=m + 3 * k)
     B = inputs.random_matrix(n if tb else k, k if tb else n, prec, seed=n + 5 * k)
     C0 = inputs.random_matrix(m, n, prec, seed=m * n)

@@ -23,7 +23,7 @@ def _cols(K, nb, n_rand=4, seed=0):
     return sorted(v for v in c if 0 <= v < K)
 
 
-@pytest.mark.parametrize("prec", ["dd", "qd", "od"])
+@pytest.mark.parametrize("prec", ["d", "dd", "qd", "od"])
 def test_invariants_config2_full(orc, mdls, dev, prec):
     M = K = 1024
     nb = 128

@@ -10,8 +10,9 @@ from fractions import Fraction
 import numpy as np
 import pytest
 
-PRECS = ["dd", "qd", "od"]
-M_OF = {"dd": 2, "qd": 4, "od": 8}
+PRECS = ["d", "dd", "qd", "od"]
+PRECS_MD = ["dd", "qd", "od"]
+M_OF = {"d": 1, "dd": 2, "qd": 4, "od": 8}
 
 
 def _md(prec, mat):
@@ -56,7 +57,7 @@ def test_inv_orth_tells_qtq_from_qqt(orc):
     assert got == max(a * a, a * b) == 2.0 ** -15  # Q Q^T would give 2^-10
 
 
-@pytest.mark.parametrize("prec", PRECS)
+@pytest.mark.parametrize("prec", PRECS_MD)  # needs > 53 bits: multi-limb only
 def test_inv_orth_hadamard_dyadic_perturbation(orc, prec):
     H = np.array([[1, 1, 1, 1], [1, -1, 1, -1], [1, 1, -1, -1], [1, -1, -1, 1]], dtype=float) / 2
     assert orc.inv_orth(prec, _md(prec, H.T)) == 0.0
@@ -66,7 +67,7 @@ def test_inv_orth_hadamard_dyadic_perturbation(orc, prec):
     assert orc.inv_orth(prec, _md(prec, Hp.T)) == d + d * d
 
 
-@pytest.mark.parametrize("prec", PRECS)
+@pytest.mark.parametrize("prec", PRECS_MD)  # needs > 53 bits: multi-limb only
 def test_inv_orth_sub_double_perturbation(orc, prec):
     """Q = I + eps E with eps = 2^-70 held in the second limb: Q^T Q - I = eps (E + E^T) + eps^2 E^T E
     is invisible to plain doubles (1 + 2^-70 rounds to 1) and is recovered only in md arithmetic."""

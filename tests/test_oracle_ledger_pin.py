@@ -36,7 +36,7 @@ def _assert_counts_equal(orc_counts, led, nonpos=0):
         assert c["div"] + (nonpos if stage == "house" else 0) == s["div"], (stage, c["div"], s["div"], nonpos)
 
 
-@pytest.mark.parametrize("prec", ["dd", "qd"])
+@pytest.mark.parametrize("prec", ["d", "dd", "qd"])
 @pytest.mark.parametrize("M,K,nb", SHAPES)
 @pytest.mark.parametrize("op", ["qr", "lstsq", "lstsq_noq", "apply_qt"])
 def test_ledger_equals_executed_counts(orc, prec, M, K, nb, op):

@@ -24,8 +24,8 @@ import pytest
 from paper_2110_08375_b200 import inputs
 
 mpmath.mp.prec = 2000
-U_OF = {"dd": 2.0 ** -104, "qd": 2.0 ** -208, "od": 2.0 ** -416}
-PRECS = ["dd", "qd", "od"]
+U_OF = {"d": 2.0 ** -53, "dd": 2.0 ** -104, "qd": 2.0 ** -208, "od": 2.0 ** -416}
+PRECS = ["d", "dd", "qd", "od"]
 
 
 def md_from(mat2d, m):

@@ -10,10 +10,10 @@ from paper_2110_08375_b200 import inputs
 
 from ._parity import U_OF
 
-M_OF = {"dd": 2, "qd": 4, "od": 8}
+M_OF = {"d": 1, "dd": 2, "qd": 4, "od": 8}
 
 
-@pytest.mark.parametrize("prec", ["dd", "qd", "od"])
+@pytest.mark.parametrize("prec", ["d", "dd", "qd", "od"])
 def test_norm2_exact_cases(orc, prec):
     m = M_OF[prec]
     y = np.zeros((m, 2))
@@ -29,7 +29,7 @@ def test_norm2_exact_cases(orc, prec):
     assert orc.norm2(prec, np.zeros((m, 0)))[0] == 0.0
 
 
-@pytest.mark.parametrize("prec", ["dd", "qd", "od"])
+@pytest.mark.parametrize("prec", ["d", "dd", "qd", "od"])
 def test_residual_spec_examples(orc, prec):
     m = M_OF[prec]
     A = np.zeros((m, 1, 2))
@@ -42,7 +42,7 @@ def test_residual_spec_examples(orc, prec):
     assert orc.residual_direct(prec, A, x, b)[0] == 1.0
 
 
-@pytest.mark.parametrize("prec", ["dd", "qd", "od"])
+@pytest.mark.parametrize("prec", ["d", "dd", "qd", "od"])
 @pytest.mark.parametrize("M,K", [(40, 12), (33, 32), (64, 8)])
 def test_tail_norm_equals_direct_residual(orc, prec, M, K):
     A, b = inputs.lstsq_problem(M, K, prec, seed=M + K)
