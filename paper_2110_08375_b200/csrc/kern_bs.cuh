@@ -1,5 +1,10 @@
 // kern_bs.cuh -- tile inversion and tiled back substitution kernels (A7-A9).
 #pragma once
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstring>
+
 #include "types.cuh"
 
 namespace mdls {
@@ -179,17 +184,45 @@ __global__ void __launch_bounds__(256) bs_mulinv_kernel(int64_t nb, int64_t tile
 // ============================================================================
 template <int M, int RB, int NS, int MINB, int NACC>
 __global__ void __launch_bounds__(256, MINB) bs_update_kernel(int64_t nb, int64_t tile, int64_t row0, int64_t row1, CMat U,
-                                                           const double* x, int64_t psx, double* b, int64_t psb) {
+                                                           const double* x, int64_t psx, double* b, int64_t psb,
+                                                           const __grid_constant__ CUtensorMap tmap, int use_tma) {
   constexpr int NT = 256, GR = NT / RB, STAGE = 2048, SC = STAGE / (M * RB);
   static_assert(SC >= GR && SC % GR == 0, "stage shape");
-  extern __shared__ double sm_bs[];
-  double* xs = sm_bs;              // M planes of nb: x_tile
-  double* ring = sm_bs + M * nb;   // NS stages of [limb][column][row]
+  extern __shared__ __align__(128) double sm_bs[];
+  double* xs = sm_bs;                                  // M planes of nb: x_tile
+  double* ring = sm_bs + ((M * nb + 15) & ~15);        // NS stages of [limb][column][row] (128-byte aligned)
   __shared__ Acc<M> part[GR][RB];
+  __shared__ __align__(8) unsigned long long full[NS];  // TMA path: stage slot filled
   const int tid = threadIdx.x, r = tid % RB, gq = tid / RB;
   const int64_t base = tile * nb, rb = row0 + (int64_t)blockIdx.x * RB;
   const int nst = (int)((nb + SC - 1) / SC);
+  // TMA path (use_tma: the host encoded a 3-D tensor map rows x columns x limb planes of U, box RB x SC x M):
+  // one cp.async.bulk.tensor per stage, issued by one thread, lands exactly in the stage's [limb][column][row]
+  // layout, zero-filled outside U, completing on the slot's mbarrier -- no per-element address arithmetic.
+  // Otherwise 8-byte cp.async (LDGSTS) per element with zero fill.
+  if (use_tma) {
+    if (tid == 0) {
+#pragma unroll
+      for (int q = 0; q < NS; ++q) mbar_init(smem_addr(&full[q]), 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("prefetch.tensormap [%0];" :: "l"(&tmap) : "memory");
+    }
+    __syncthreads();
+  }
   auto issue = [&](int st) {
+    if (use_tma) {
+      if (st < nst && tid == 0) {
+        const int slot = st % NS;
+        const uint32_t bar = smem_addr(&full[slot]);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the slot's earlier generic reads first
+        mbar_arm(bar, (uint32_t)(STAGE * sizeof(double)));
+        const int c0 = (int)rb, c1 = (int)(base + (int64_t)st * SC), c2 = 0;
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+            :: "r"(smem_addr(ring + slot * STAGE)), "l"(&tmap), "r"(c0), "r"(c1), "r"(c2), "r"(bar) : "memory");
+      }
+      return;
+    }
     if (st < nst) {
       double* dst = ring + (st % NS) * STAGE;
       for (int e = tid; e < STAGE; e += NT) {
@@ -209,12 +242,13 @@ __global__ void __launch_bounds__(256, MINB) bs_update_kernel(int64_t nb, int64_
 #pragma unroll
     for (int k = 0; k < M; ++k) xs[k * nb + e] = x[k * psx + base + e];
   constexpr int CPT = SC / GR;  // columns per thread per stage
-  Acc<M> acc0, acc1;             // two independent chains (alternate columns), merged at the end
-  acc0.init();
-  acc1.init();
+  Acc<M> acc[NACC];              // NACC independent chains (round-robin over the thread's columns), merged at the end
+#pragma unroll
+  for (int a = 0; a < NACC; ++a) acc[a].init();
   for (int st = 0; st < nst; ++st) {
-    cp_async_wait<NS - 2>();  // this thread's copies of stage st have landed
-    __syncthreads();          // everyone's; and stage st - 1 is consumed, its slot free
+    if (use_tma) mbar_wait(smem_addr(&full[st % NS]), (uint32_t)((st / NS) & 1));  // stage st has landed
+    else cp_async_wait<NS - 2>();  // this thread's copies of stage st have landed
+    __syncthreads();               // everyone's; and stage st - 1 is consumed, its slot free
     issue(st + NS - 1);
     const double* sg = ring + (st % NS) * STAGE;
 #pragma unroll
@@ -228,14 +262,25 @@ __global__ void __launch_bounds__(256, MINB) bs_update_kernel(int64_t nb, int64_
           u.v[k] = sg[(k * SC + c) * RB + r];
           xx.v[k] = xs[k * nb + col];
         }
-        if (NACC == 2 && ((st * CPT + j) & 1)) acc1.add_prod(u, xx);  // warp-uniform
-        else acc0.add_prod(u, xx);
+        // chain (st CPT + j) mod NACC: j is a compile-time constant, the stage parity a warp-uniform branch
+        // (constant indices only, so the chains stay in registers)
+        if constexpr (NACC == 1) {
+          acc[0].add_prod(u, xx);
+        } else if constexpr (CPT % NACC == 0) {
+          acc[j % NACC].add_prod(u, xx);
+        } else {
+          const int sel = (int)((st * CPT) % NACC);
+#pragma unroll
+          for (int a = 0; a < NACC; ++a)
+            if (sel == a) acc[(a + j) % NACC].add_prod(u, xx);
+        }
       }
     }
   }
   cp_async_wait<0>();
-  acc0.merge(acc1);
-  part[gq][r] = acc0;
+#pragma unroll
+  for (int a = 1; a < NACC; ++a) acc[0].merge(acc[a]);
+  part[gq][r] = acc[0];
   __syncthreads();
   // fixed-order tree over the column groups (exact accumulator merges)
 #pragma unroll
@@ -288,6 +333,35 @@ void launch_bs_mulinv(cudaStream_t st, int64_t nb, int64_t tile, CMat Vt, const 
   else MDLS_LAUNCH(F_BS, st, launch_pdl(bs_mulinv_kernel<M, 8>, grid, dim3(256), 0, st, nb, tile, Vt, b, psb, x, psx));
 }
 
+// 3-D tensor map of U for the update kernel's TMA stages: dims (rows, columns, limb planes), strides
+// (ld, ps) doubles, box (RB, SC, M); 0 (use the LDGSTS path) when the operand is not 16-byte aligned, the
+// driver entry point is missing, encoding fails, or MDLS_BS_TMA=0
+inline int64_t base_cols_end(int64_t nb, int64_t tile) { return (tile + 1) * nb; }
+inline int bs_tensor_map(CUtensorMap* tm, CMat U, int64_t rows, int64_t cols, int M, int RB, int SC) {
+  static const bool env_on = [] {
+    const char* v = getenv("MDLS_BS_TMA");
+    return !(v && v[0] == '0');
+  }();
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  std::memset(tm, 0, sizeof(*tm));
+  if (!env_on || !encode || (U.ld % 2) || (U.ps % 2) || ((uintptr_t)U.p & 15)) return 0;
+  const cuuint64_t dims[3] = {(cuuint64_t)rows, (cuuint64_t)cols, (cuuint64_t)M};
+  const cuuint64_t strides[2] = {(cuuint64_t)U.ld * sizeof(double), (cuuint64_t)U.ps * sizeof(double)};
+  const cuuint32_t box[3] = {(cuuint32_t)RB, (cuuint32_t)SC, (cuuint32_t)M};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult rc = encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(U.p), dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return rc == CUDA_SUCCESS ? 1 : 0;
+}
+
 // rows [row0, row1): RB = 32 rows per CTA when that still gives two CTAs per SM, else RB = 8;
 // NS stages of 16 KB (dynamic shared memory beyond 48 KB: attribute set once per device)
 template <int M, int RB, int NS, int MINB, int NACC>
@@ -295,17 +369,20 @@ void bs_update_launch(cudaStream_t st, int64_t nb, int64_t tile, int64_t row0, i
                       int64_t psx, double* b, int64_t psb) {
   static bool attr_set[kMaxDev];
   const int dev = cur_dev();
-  const size_t smem = sizeof(double) * ((size_t)M * nb + (size_t)NS * 2048);
+  const size_t smem = sizeof(double) * ((((size_t)M * nb + 15) & ~(size_t)15) + (size_t)NS * 2048);
   if (!attr_set[dev]) {
     cudaFuncSetAttribute(bs_update_kernel<M, RB, NS, MINB, NACC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(sizeof(double) * ((size_t)M * 256 + (size_t)NS * 2048)));
+                         (int)(sizeof(double) * ((size_t)M * 256 + 16 + (size_t)NS * 2048)));
     attr_set[dev] = true;
   }
+  CUtensorMap tm;
+  const int use_tma = bs_tensor_map(&tm, U, row1, base_cols_end(nb, tile), M, RB, 2048 / (M * RB));
   MDLS_LAUNCH(F_BS, st, launch_pdl(bs_update_kernel<M, RB, NS, MINB, NACC>, dim3((unsigned)cdiv(row1 - row0, RB)),
-                                    dim3(256), smem, st, nb, tile, row0, row1, U, x, psx, b, psb));
+                                    dim3(256), smem, st, nb, tile, row0, row1, U, x, psx, b, psb, tm, use_tma));
 }
 // variant (MDLS_BSU): 0 = NS 4, two CTAs per SM, two accumulator chains per thread (default, measured
-// 4.44 ms at config 4); 1 = the same with one chain (4.52 ms); 2 = NS 3, three CTAs per SM, two chains (5.17)
+// 4.44 ms at config 4); 1 = the same with one chain (4.52 ms); 2 = NS 3, three CTAs per SM, two chains (5.17);
+// 3 = NS 4, two CTAs per SM, four chains
 
 template <int M, int RB>
 void bs_update_variant(cudaStream_t st, int64_t nb, int64_t tile, int64_t row0, int64_t row1, CMat U, const double* x,
@@ -315,6 +392,7 @@ void bs_update_variant(cudaStream_t st, int64_t nb, int64_t tile, int64_t row0, 
     return e ? atoi(e) : 0;
   }();
   if (v == 1) bs_update_launch<M, RB, 4, 2, 1>(st, nb, tile, row0, row1, U, x, psx, b, psb);
+  else if (v == 3) bs_update_launch<M, RB, 4, 2, 4>(st, nb, tile, row0, row1, U, x, psx, b, psb);
   else if (v == 2) bs_update_launch<M, RB, 3, 3, 2>(st, nb, tile, row0, row1, U, x, psx, b, psb);
   else bs_update_launch<M, RB, 4, 2, 2>(st, nb, tile, row0, row1, U, x, psx, b, psb);
 }

@@ -444,7 +444,6 @@ struct HalveAcc<M, V, 0, TPR> {
 };
 
 // --- async DSMEM helpers (st.async + mbarrier complete_tx) ---
-__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ uint32_t cluster_addr(uint32_t a, int rank) {
   uint32_t r;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
@@ -453,19 +452,6 @@ __device__ __forceinline__ uint32_t cluster_addr(uint32_t a, int rank) {
 __device__ __forceinline__ void st_async_v2(uint32_t raddr, double x, double y, uint32_t rbar) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];"
                :: "r"(raddr), "d"(x), "d"(y), "r"(rbar) : "memory");
-}
-__device__ __forceinline__ void mbar_init(uint32_t bar, int count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arm(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n"
-      "MDLS_WAIT_%=:\n"
-      " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra MDLS_WAIT_%=;\n}\n" :: "r"(bar), "r"(parity) : "memory");
 }
 __device__ __forceinline__ void st_async_f64(uint32_t raddr, double x, uint32_t rbar) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];"
