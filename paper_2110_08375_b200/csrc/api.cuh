@@ -143,7 +143,7 @@ int MDLS_FN(mdls_backsub_)(int64_t n, int64_t nb, const double* U, int64_t ldu, 
   int* slot = at<int>(work, p.info);
   MDLS_LAUNCH(F_MISC, st, info_init_kernel<<<1, 1, 0, st>>>(slot));
   backsub<M>(st, n, nb, CMat{U, ldu, psu}, y, psy, x, psx, Mat{at<double>(work, p.vt), nb, nb * n},
-             Mat{at<double>(work, p.us), nb, nb * n}, at<double>(work, p.v0), slot);
+             Mat{at<double>(work, p.us), nb, nb * n}, at<double>(work, p.v0), slot, at<int>(work, p.flags));
   if (dev_info) MDLS_LAUNCH(F_MISC, st, info_finish_kernel<<<1, 1, 0, st>>>(slot, nullptr, dev_info));
   return launched();
 }
@@ -207,7 +207,7 @@ static int lstsq_run(cudaStream_t st, int64_t Mr, int64_t K, int64_t nb, const d
     apply_qt_panels<M>(st, Mr, K, nb, cm(bb.Y), cm(bb.W), Mat{yv, Mr, Mr}, bb.X, bb.part, bb.part_cap);
   }
   backsub<M>(st, K, nb, cm(Af), yv, Mr, x, psx, Mat{at<double>(work, p.vt), nb, nb * K},
-             Mat{at<double>(work, p.us), nb, nb * K}, at<double>(work, p.v0), bb.info_slot);
+             Mat{at<double>(work, p.us), nb, nb * K}, at<double>(work, p.v0), bb.info_slot, at<int>(work, p.flags));
   set_stage(MDLS_NSTAGES);
   if (R_out) MDLS_LAUNCH(F_MISC, st, copy_kernel<M><<<grid_for(Mr * K, 256), 256, 0, st>>>(Mr, K, cm(Af), Mat{R_out, ldr, psr}, 1));
   if (y_out) MDLS_LAUNCH(F_MISC, st, copy_kernel<M><<<grid_for(Mr, 256), 256, 0, st>>>(Mr, 1, CMat{yv, Mr, Mr}, Mat{y_out, Mr, psy}, 0));

@@ -135,25 +135,35 @@ __global__ void __launch_bounds__(256) invert_tiles_kernel(int64_t nb, CMat U, C
 // ============================================================================
 template <int M, int NPL>
 __global__ void __launch_bounds__(256) bs_mulinv_kernel(int64_t nb, int64_t tile, CMat Vt, const double* b,
-                                                        int64_t psb, double* x, int64_t psx) {
+                                                        int64_t psb, double* x, int64_t psx, BsFlow fl, int first) {
   pdl_trigger();
   const int lane = threadIdx.x & 31;
   const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const bool live = r < nb;
   const int64_t base = tile * nb;
   // the lane's columns c = r + lane + 32 t (upper triangular: c >= r), every load issued before any product;
-  // the inverse (complete: a full dependency) before the PDL wait, b (the predecessor's output) after it
+  // the inverse (complete: a full dependency) before waiting, b (the updates' output) after
   md<M> tv[NPL], bv[NPL];
 #pragma unroll
   for (int t = 0; t < NPL; ++t) {
     const int64_t c = r + lane + 32 * t;
-    tv[t] = (r < nb && c < nb) ? ld<M>(Vt.p, Vt.ps, c + (base + r) * Vt.ld) : md_zero<M>();
+    tv[t] = (live && c < nb) ? ld<M>(Vt.p, Vt.ps, c + (base + r) * Vt.ld) : md_zero<M>();
   }
-  pdl_wait();
-  if (r >= nb) return;
+  if (fl.rows && !first) {
+    // dataflow: b_tile final once every later step's update reached its nb rows
+    if (threadIdx.x == 0) spin_geq(fl.rows + tile, (int)(nb * (fl.N - 1 - tile)));
+    __syncthreads();
+  } else {
+    pdl_wait();
+  }
 #pragma unroll
   for (int t = 0; t < NPL; ++t) {
     const int64_t c = r + lane + 32 * t;
-    bv[t] = (c < nb) ? ld<M>(b, psb, base + c) : md_zero<M>();
+    md<M> v = md_zero<M>();
+    if (live && c < nb)
+#pragma unroll
+      for (int k = 0; k < M; ++k) v.v[k] = __ldcg(b + k * psb + base + c);
+    bv[t] = v;
   }
   Acc<M> acc, acc2;  // two independent chains (even / odd t), merged before the tree
   acc.init();
@@ -167,7 +177,18 @@ __global__ void __launch_bounds__(256) bs_mulinv_kernel(int64_t nb, int64_t tile
   // fixed-order tree of exact accumulator merges (no renormalised md add per level)
 #pragma unroll
   for (int d = 16; d >= 1; d >>= 1) acc.merge(acc_shfl_down<M>(acc, d));
-  if (lane == 0) st<M>(x, psx, base + r, acc.get());
+  if (lane == 0 && live) {
+    st<M>(x, psx, base + r, acc.get());
+    if (fl.rows) __threadfence();
+  }
+  if (fl.rows) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int64_t r0 = (int64_t)blockIdx.x * (blockDim.x >> 5);
+      const int64_t r1 = r0 + (blockDim.x >> 5), rows = (r1 < nb ? r1 : nb) - r0;
+      red_release_gpu(fl.xrdy + tile, (int)rows);  // x_tile rows published
+    }
+  }
 }
 
 // ============================================================================
@@ -185,7 +206,8 @@ __global__ void __launch_bounds__(256) bs_mulinv_kernel(int64_t nb, int64_t tile
 template <int M, int RB, int NS, int MINB, int NACC>
 __global__ void __launch_bounds__(256, MINB) bs_update_kernel(int64_t nb, int64_t tile, int64_t row0, int64_t row1, CMat U,
                                                            const double* x, int64_t psx, double* b, int64_t psb,
-                                                           const __grid_constant__ CUtensorMap tmap, int use_tma) {
+                                                           const __grid_constant__ CUtensorMap tmap, int use_tma,
+                                                           BsFlow fl) {
   constexpr int NT = 256, GR = NT / RB, STAGE = 2048, SC = STAGE / (M * RB);
   static_assert(SC >= GR && SC % GR == 0, "stage shape");
   extern __shared__ __align__(128) double sm_bs[];
@@ -194,7 +216,9 @@ __global__ void __launch_bounds__(256, MINB) bs_update_kernel(int64_t nb, int64_
   __shared__ Acc<M> part[GR][RB];
   __shared__ __align__(8) unsigned long long full[NS];  // TMA path: stage slot filled
   const int tid = threadIdx.x, r = tid % RB, gq = tid / RB;
-  const int64_t base = tile * nb, rb = row0 + (int64_t)blockIdx.x * RB;
+  const int64_t base = tile * nb;
+  // dataflow mode: row blocks from the diagonal upward (the critical tile first); launch order otherwise
+  const int64_t rb = fl.rows ? row1 - (int64_t)(blockIdx.x + 1) * RB : row0 + (int64_t)blockIdx.x * RB;
   const int nst = (int)((nb + SC - 1) / SC);
   // TMA path (use_tma: the host encoded a 3-D tensor map rows x columns x limb planes of U, box RB x SC x M):
   // one cp.async.bulk.tensor per stage, issued by one thread, lands exactly in the stage's [limb][column][row]
@@ -237,10 +261,19 @@ __global__ void __launch_bounds__(256, MINB) bs_update_kernel(int64_t nb, int64_
   pdl_trigger();
 #pragma unroll
   for (int st = 0; st < NS - 1; ++st) issue(st);  // U is read-only here: prefetched before the PDL wait
-  pdl_wait();                                     // x (mulinv) and b (the previous update) from here on
+  if (fl.rows) {
+    // dataflow: x_tile written (mulinv) and this row block's tile updated by every later step
+    if (tid == 0) {
+      spin_geq(fl.xrdy + tile, (int)nb);
+      spin_geq(fl.rows + rb / nb, (int)(nb * (fl.N - 1 - tile)));
+    }
+    __syncthreads();
+  } else {
+    pdl_wait();  // x (mulinv) and b (the previous update) from here on
+  }
   for (int64_t e = tid; e < nb; e += NT)
 #pragma unroll
-    for (int k = 0; k < M; ++k) xs[k * nb + e] = x[k * psx + base + e];
+    for (int k = 0; k < M; ++k) xs[k * nb + e] = __ldcg(x + k * psx + base + e);
   constexpr int CPT = SC / GR;  // columns per thread per stage
   Acc<M> acc[NACC];              // NACC independent chains (round-robin over the thread's columns), merged at the end
 #pragma unroll
@@ -294,8 +327,15 @@ __global__ void __launch_bounds__(256, MINB) bs_update_kernel(int64_t nb, int64_
   }
   if (gq == 0 && rb + r < row1) {
     const md<M> t = part[0][r].get();
-    const md<M> bb = ld<M>(b, psb, rb + r);
+    md<M> bb;
+#pragma unroll
+    for (int k = 0; k < M; ++k) bb.v[k] = __ldcg(b + k * psb + rb + r);
     st<M>(b, psb, rb + r, add<M>(bb, neg(t)));
+    if (fl.rows) __threadfence();
+  }
+  if (fl.rows) {
+    __syncthreads();
+    if (tid == 0) red_release_gpu(fl.rows + rb / nb, RB);  // this block's rows of the tile updated
   }
 }
 
@@ -326,11 +366,11 @@ void launch_invert(cudaStream_t st, int64_t ntiles, int64_t nb, CMat U, Mat Vt, 
 
 template <int M>
 void launch_bs_mulinv(cudaStream_t st, int64_t nb, int64_t tile, CMat Vt, const double* b, int64_t psb, double* x,
-                      int64_t psx) {
+                      int64_t psx, BsFlow fl, bool first) {
   const dim3 grid((unsigned)cdiv(nb, 8));
-  if (nb <= 64) MDLS_LAUNCH(F_BS, st, launch_pdl(bs_mulinv_kernel<M, 2>, grid, dim3(256), 0, st, nb, tile, Vt, b, psb, x, psx));
-  else if (nb <= 128) MDLS_LAUNCH(F_BS, st, launch_pdl(bs_mulinv_kernel<M, 4>, grid, dim3(256), 0, st, nb, tile, Vt, b, psb, x, psx));
-  else MDLS_LAUNCH(F_BS, st, launch_pdl(bs_mulinv_kernel<M, 8>, grid, dim3(256), 0, st, nb, tile, Vt, b, psb, x, psx));
+  if (nb <= 64) MDLS_LAUNCH(F_BS, st, launch_pdl(bs_mulinv_kernel<M, 2>, grid, dim3(256), 0, st, nb, tile, Vt, b, psb, x, psx, fl, (int)first));
+  else if (nb <= 128) MDLS_LAUNCH(F_BS, st, launch_pdl(bs_mulinv_kernel<M, 4>, grid, dim3(256), 0, st, nb, tile, Vt, b, psb, x, psx, fl, (int)first));
+  else MDLS_LAUNCH(F_BS, st, launch_pdl(bs_mulinv_kernel<M, 8>, grid, dim3(256), 0, st, nb, tile, Vt, b, psb, x, psx, fl, (int)first));
 }
 
 // 3-D tensor map of U for the update kernel's TMA stages: dims (rows, columns, limb planes), strides
@@ -366,7 +406,7 @@ inline int bs_tensor_map(CUtensorMap* tm, CMat U, int64_t rows, int64_t cols, in
 // NS stages of 16 KB (dynamic shared memory beyond 48 KB: attribute set once per device)
 template <int M, int RB, int NS, int MINB, int NACC>
 void bs_update_launch(cudaStream_t st, int64_t nb, int64_t tile, int64_t row0, int64_t row1, CMat U, const double* x,
-                      int64_t psx, double* b, int64_t psb) {
+                      int64_t psx, double* b, int64_t psb, BsFlow fl) {
   static bool attr_set[kMaxDev];
   const int dev = cur_dev();
   const size_t smem = sizeof(double) * ((((size_t)M * nb + 15) & ~(size_t)15) + (size_t)NS * 2048);
@@ -378,7 +418,7 @@ void bs_update_launch(cudaStream_t st, int64_t nb, int64_t tile, int64_t row0, i
   CUtensorMap tm;
   const int use_tma = bs_tensor_map(&tm, U, row1, base_cols_end(nb, tile), M, RB, 2048 / (M * RB));
   MDLS_LAUNCH(F_BS, st, launch_pdl(bs_update_kernel<M, RB, NS, MINB, NACC>, dim3((unsigned)cdiv(row1 - row0, RB)),
-                                    dim3(256), smem, st, nb, tile, row0, row1, U, x, psx, b, psb, tm, use_tma));
+                                    dim3(256), smem, st, nb, tile, row0, row1, U, x, psx, b, psb, tm, use_tma, fl));
 }
 // variant (MDLS_BSU): 0 = NS 4, two CTAs per SM, two accumulator chains per thread (default, measured
 // 4.44 ms at config 4); 1 = the same with one chain (4.52 ms); 2 = NS 3, three CTAs per SM, two chains (5.17);
@@ -386,30 +426,30 @@ void bs_update_launch(cudaStream_t st, int64_t nb, int64_t tile, int64_t row0, i
 
 template <int M, int RB>
 void bs_update_variant(cudaStream_t st, int64_t nb, int64_t tile, int64_t row0, int64_t row1, CMat U, const double* x,
-                       int64_t psx, double* b, int64_t psb) {
+                       int64_t psx, double* b, int64_t psb, BsFlow fl) {
   static const int v = [] {
     const char* e = getenv("MDLS_BSU");
     return e ? atoi(e) : 0;
   }();
-  if (v == 1) bs_update_launch<M, RB, 4, 2, 1>(st, nb, tile, row0, row1, U, x, psx, b, psb);
-  else if (v == 3) bs_update_launch<M, RB, 4, 2, 4>(st, nb, tile, row0, row1, U, x, psx, b, psb);
-  else if (v == 2) bs_update_launch<M, RB, 3, 3, 2>(st, nb, tile, row0, row1, U, x, psx, b, psb);
-  else bs_update_launch<M, RB, 4, 2, 2>(st, nb, tile, row0, row1, U, x, psx, b, psb);
+  if (v == 1) bs_update_launch<M, RB, 4, 2, 1>(st, nb, tile, row0, row1, U, x, psx, b, psb, fl);
+  else if (v == 3) bs_update_launch<M, RB, 4, 2, 4>(st, nb, tile, row0, row1, U, x, psx, b, psb, fl);
+  else if (v == 2) bs_update_launch<M, RB, 3, 3, 2>(st, nb, tile, row0, row1, U, x, psx, b, psb, fl);
+  else bs_update_launch<M, RB, 4, 2, 2>(st, nb, tile, row0, row1, U, x, psx, b, psb, fl);
 }
 template <int M>
 void launch_bs_update(cudaStream_t st, int64_t nb, int64_t tile, int64_t row0, int64_t row1, CMat U, const double* x,
-                      int64_t psx, double* b, int64_t psb) {
+                      int64_t psx, double* b, int64_t psb, BsFlow fl) {
   const int64_t rows = row1 - row0;
   if (rows <= 0) return;
-  if (cdiv(rows, 32) >= 2 * num_sms()) bs_update_variant<M, 32>(st, nb, tile, row0, row1, U, x, psx, b, psb);
-  else bs_update_variant<M, 8>(st, nb, tile, row0, row1, U, x, psx, b, psb);
+  if (cdiv(rows, 32) >= 2 * num_sms()) bs_update_variant<M, 32>(st, nb, tile, row0, row1, U, x, psx, b, psb, fl);
+  else bs_update_variant<M, 8>(st, nb, tile, row0, row1, U, x, psx, b, psb, fl);
 }
 
 #define MDLS_INSTANTIATE_BS(MM)                                                                                \
   template void launch_invert<MM>(cudaStream_t, int64_t, int64_t, CMat, Mat, Mat, int*, int64_t);                                     \
   template void launch_bs_mulinv<MM>(cudaStream_t, int64_t, int64_t, CMat, const double*, int64_t, double*,    \
-                                     int64_t);                                                                 \
+                                     int64_t, BsFlow, bool);                                                   \
   template void launch_bs_update<MM>(cudaStream_t, int64_t, int64_t, int64_t, int64_t, CMat, const double*,  \
-                                     int64_t, double*, int64_t);
+                                     int64_t, double*, int64_t, BsFlow);
 
 }  // namespace mdls

@@ -44,15 +44,24 @@ template <int M>
 cudaError_t launch_leaf_chain(cudaStream_t st, int64_t Mrows, int64_t js, int B, Mat A, Mat Y, double* beta,
                               int64_t bps, Mat T, int* info, Mat Tp, int64_t jsp);
 
+// the dataflow back substitution needs every row block of both update-kernel shapes inside one tile
+template <int M>
+inline bool bs_flow_ok(int64_t n, int64_t nb) {
+  static const bool on = [] {
+    const char* v = getenv("MDLS_BS_FLOW");
+    return !(v && v[0] == '0');
+  }();
+  return on && nb % 32 == 0 && n % nb == 0;
+}
 template <int M>
 void launch_invert(cudaStream_t st, int64_t ntiles, int64_t nb, CMat U, Mat Vt, Mat Us, int* info, int64_t info_off);
 
 template <int M>
 void launch_bs_mulinv(cudaStream_t st, int64_t nb, int64_t tile, CMat Vt, const double* b, int64_t psb, double* x,
-                      int64_t psx);
+                      int64_t psx, BsFlow fl, bool first);
 
 template <int M>
 void launch_bs_update(cudaStream_t st, int64_t nb, int64_t tile, int64_t row0, int64_t row1, CMat U, const double* x,
-                      int64_t psx, double* b, int64_t psb);
+                      int64_t psx, double* b, int64_t psb, BsFlow fl);
 
 }  // namespace mdls

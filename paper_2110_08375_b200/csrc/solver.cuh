@@ -25,7 +25,7 @@ namespace mdls {
 // ---------------------------------------------------------------------------
 struct Plan {
   size_t af = 0, q = 0, y = 0, w = 0, beta = 0, s = 0, t = 0, x = 0, part = 0, v0 = 0, v1 = 0, v2 = 0, vt = 0, us = 0,
-         info = 0, total = 0;
+         flags = 0, info = 0, total = 0;
 };
 
 // md elements of one lane's split-K / stream-K partial buffer: kMaxSplit nb x max(M, K) partials, or the
@@ -67,6 +67,7 @@ Plan make_plan(int op, int64_t Mr, int64_t K, int64_t nb) {
   if (op == MDLS_OP_BACKSUB || op == MDLS_OP_LSTSQ || op == MDLS_OP_LSTSQ_NOQ) {
     p.vt = take(md * nb * K);
     p.us = take(md * nb * K);  // row-scaled diagonal tiles (tile inversion)
+    p.flags = take(2 * sizeof(int) * (size_t)K);  // back-substitution dataflow counters (rows updated / x rows)
   }
   p.info = take(4 * sizeof(int));
   p.total = off;
@@ -471,7 +472,7 @@ void apply_qt_panels(cudaStream_t st, int64_t Mr, int64_t K, int64_t nb, CMat Y,
 // as the bottom chunk is inverted.
 template <int M>
 void backsub(cudaStream_t st, int64_t n, int64_t nb, CMat U, const double* y, int64_t psy, double* x, int64_t psx,
-             Mat Vt, Mat Us, double* bwork, int* info_slot) {
+             Mat Vt, Mat Us, double* bwork, int* info_slot, int* flags) {
   const int64_t N = n / nb;
   cudaStream_t sinv = side_stream(3), sch = side_stream(0);
   auto fork = [](cudaStream_t from, cudaStream_t to) {
@@ -499,6 +500,13 @@ void backsub(cudaStream_t st, int64_t n, int64_t nb, CMat U, const double* y, in
     cudaEventRecord(ev, sinv);
     for (int64_t t = lo; t < hi; ++t) inv_ready[(size_t)t] = ev;
   }
+  // dataflow counters (bs_flow_ok): rows of tile j updated so far / entries of x_i written
+  BsFlow fl{nullptr, nullptr, N};
+  if (flags && bs_flow_ok<M>(n, nb)) {
+    fl.rows = flags;
+    fl.xrdy = flags + N;
+    cudaMemsetAsync(flags, 0, sizeof(int) * 2 * (size_t)N, sch);
+  }
   // bwork = y (n entries)
   MDLS_LAUNCH(F_MISC, sch, copy_kernel<M><<<grid_for(n, 256), 256, 0, sch>>>(n, 1, CMat{y, n, psy}, Mat{bwork, n, n}, 0));
   cudaEvent_t waited = nullptr;
@@ -508,9 +516,9 @@ void backsub(cudaStream_t st, int64_t n, int64_t nb, CMat U, const double* y, in
       waited = inv_ready[(size_t)i];
     }
     set_stage(MDLS_ST_MULINV);
-    launch_bs_mulinv<M>(sch, nb, i, cm(Vt), bwork, n, x, psx);
+    launch_bs_mulinv<M>(sch, nb, i, cm(Vt), bwork, n, x, psx, fl, i == N - 1);
     set_stage(MDLS_ST_BSUPDATE);
-    if (i >= 1) launch_bs_update<M>(sch, nb, i, 0, i * nb, U, x, psx, bwork, n);
+    if (i >= 1) launch_bs_update<M>(sch, nb, i, 0, i * nb, U, x, psx, bwork, n, fl);
   }
   fork(sinv, st);
   fork(sch, st);

@@ -148,6 +148,24 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
       " @!p bra MDLS_WAIT_%=;\n}\n" :: "r"(bar), "r"(parity) : "memory");
 }
+// back-substitution dataflow counters (solver.cuh::backsub): rows[j] = rows of tile j updated so far
+// (nb per chain step), xrdy[i] = entries of x_i written; null rows = launch-ordered (PDL wait) mode
+struct BsFlow {
+  int* rows;
+  int* xrdy;
+  int64_t N;
+};
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_gpu(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void spin_geq(const int* p, int target) {
+  while (ld_acquire_gpu(p) < target) __nanosleep(20);
+}
 // one-dimensional bulk copy global -> shared (TMA engine, UBLKCP): 16-byte aligned, size a multiple of 16;
 // completes `bytes` on the mbarrier `bar` (armed by mbar_arm)
 __device__ __forceinline__ void bulk_copy_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
