@@ -1,4 +1,4 @@
-"""The opt-in factorisation variants stay correct:
+"""The opt-in factorisation and back-substitution variants stay correct:
 persistent leaf chain (MDLS_PERSIST=1), one-launch leaf trailing update
 (MDLS_FUSED_APPLY=1), GEMM next-leaf apply (MDLS_PROLOGUE=0), the GEMM-chained
 panel path (MDLS_CHAIN=0) and the shared-memory leaf (MDLS_LEAF=smem).  The
@@ -51,3 +51,12 @@ def test_variant_parity(orc, tmp_path, env, prec, M, nb):
     err, tol = vec_ok(orc, prec, np.load(xout), xo, M)
     assert err <= tol, (env, err, tol)
     assert mat_cols_ok(orc, prec, np.load(rout), Ro, M) <= 1.0
+
+
+@pytest.mark.parametrize("env", [{"MDLS_BS_FLOW": "0"}, {"MDLS_BS_TMA": "0"}, {"MDLS_PDL": "0"}, {"MDLS_BSU": "1"},
+                                 {"MDLS_BSU": "2"}, {"MDLS_BSU": "3"}])
+@pytest.mark.parametrize("prec,M,nb", [("dd", 256, 32), ("qd", 256, 64)])
+def test_chain_variant_parity(orc, tmp_path, env, prec, M, nb):
+    """launch-ordered back substitution, LDGSTS staging, no programmatic dependent launch, the update-kernel
+    shapes of MDLS_BSU: x and R at the north_star tolerance"""
+    test_variant_parity(orc, tmp_path, env, prec, M, nb)
