@@ -1,7 +1,7 @@
 """The opt-in factorisation and back-substitution variants stay correct:
-persistent leaf chain (MDLS_PERSIST=1), one-launch leaf trailing update
-(MDLS_FUSED_APPLY=1), GEMM next-leaf apply (MDLS_PROLOGUE=0), the GEMM-chained
-panel path (MDLS_CHAIN=0) and the shared-memory leaf (MDLS_LEAF=smem).  The
+the GEMM-chained panel path (MDLS_CHAIN=0), the shared-memory leaf (MDLS_LEAF=smem), backward Q for dd
+(MDLS_QFORM=backward), split-K instead of stream-K (MDLS_STREAMK=0), per-leaf updates of every column
+(MDLS_DEFER=0) and 8-CTA leaf clusters (MDLS_LEAF_C=8).  The
 switches are read once per process, so each runs in a fresh interpreter; x and R
 are compared with the oracle at the north_star tolerance."""
 import json
@@ -36,8 +36,8 @@ print(json.dumps({{"info": int(r.info.item())}}))
 """
 
 
-@pytest.mark.parametrize("env", [{"MDLS_PERSIST": "1"}, {"MDLS_FUSED_APPLY": "1"}, {"MDLS_PROLOGUE": "0"},
-                                 {"MDLS_CHAIN": "0"}, {"MDLS_LEAF": "smem", "MDLS_CHAIN": "0"}])
+@pytest.mark.parametrize("env", [{"MDLS_CHAIN": "0"}, {"MDLS_LEAF": "smem", "MDLS_CHAIN": "0"}, {"MDLS_QFORM": "backward"},
+                                 {"MDLS_STREAMK": "0"}, {"MDLS_DEFER": "0"}, {"MDLS_LEAF_C": "8"}])
 @pytest.mark.parametrize("prec,M,nb", [("dd", 256, 32), ("qd", 128, 16)])
 def test_variant_parity(orc, tmp_path, env, prec, M, nb):
     xout, rout = str(tmp_path / "x.npy"), str(tmp_path / "R.npy")
