@@ -49,8 +49,9 @@ FP64_PIPE_TOPS = 148 * 64 * 1.965e9 / 1e12            # 18.6 FP64-pipe lane ops/
 # sum_{n<=M-2} (n+1) [two_prod + exact deposits] = 115 / 967, + the per-k-tile bin renormalisation)
 OPS_PER_PAIR = {"d": 1, "dd": 12, "qd": 116, "od": 970}
 # dram traffic per launch of the roofline GEMM (1024 x 1024 x 128, C += X Y^T) from one ncu --set full
-# capture (tools/prof_gemm.py; dd: profiles/r02_ncu_final.txt, stream-K; qd/od: profiles/r01_ncu_gemm_roofline.txt)
-GEMM_NCU_TRAFFIC = {"dd": 21080064 + 23296, "qd": 42001664 + 119040, "od": 84171776 + 14920192}
+# capture (tools/prof_gemm.py; dd: profiles/r02_ncu_final_c.txt, 64 x 32 tiles, split-K 4 -- the write is the
+# split-K partials; qd/od: profiles/r01_ncu_gemm_roofline.txt)
+GEMM_NCU_TRAFFIC = {"dd": 4259840 + 9678336, "qd": 42001664 + 119040, "od": 84171776 + 14920192}
 # paper's V100 times for the same least-squares workload (T11): QR + BS kernel ms
 PAPER_V100_MS = {"dd": 451.1 + 4.0, "qd": 3020.6 + 28.0, "od": 11924.5 + 114.5}
 L2_FLUSH_BYTES = 512 << 20

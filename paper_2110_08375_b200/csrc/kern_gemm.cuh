@@ -41,7 +41,7 @@ struct GemmSmem {
 };
 
 template <int M, int V, bool TA, bool TB>
-__global__ void __launch_bounds__(GemmTile<M, V>::NT) gemm_kernel(GemmArgs g) {
+__global__ void __launch_bounds__(GemmTile<M, V>::NT, GemmTile<M, V>::MINB) gemm_kernel(GemmArgs g) {
   using Tl = GemmTile<M, V>;
   using Sm = GemmSmem<M, V, TA, TB>;
   constexpr int BM = Tl::BM, BN = Tl::BN, BK = Tl::BK;

@@ -190,9 +190,9 @@ inline CMat sub(const CMat& a, int64_t i, int64_t j) { return CMat{a.p + i + j *
 
 // md GEMM tile variants: <BM, BN, BK, TM, TN>; V = 0 large, 1 medium, 2 skinny-m
 // (few output rows, e.g. W^T C), 3 skinny-n (few output columns, e.g. Q^T b)
-template <int BM_, int BN_, int BK_, int TM_, int TN_>
+template <int BM_, int BN_, int BK_, int TM_, int TN_, int MINB_ = 1>
 struct Tile {
-  static constexpr int BM = BM_, BN = BN_, BK = BK_, TM = TM_, TN = TN_;
+  static constexpr int BM = BM_, BN = BN_, BK = BK_, TM = TM_, TN = TN_, MINB = MINB_;  // MINB: CTAs per SM
   static constexpr int NT = (BM / TM) * (BN / TN);
 };
 template <int M, int V>
@@ -202,7 +202,9 @@ template <> struct GemmTile<1, 0> : Tile<64, 64, 16, 4, 4> {};
 template <> struct GemmTile<1, 1> : Tile<32, 32, 16, 2, 2> {};
 template <> struct GemmTile<1, 2> : Tile<16, 64, 16, 1, 4> {};
 template <> struct GemmTile<1, 3> : Tile<64, 16, 16, 4, 1> {};
-template <> struct GemmTile<2, 0> : Tile<64, 64, 16, 4, 4> {};
+// dd large tile 64 x 32, 4 x 2 outputs per thread, 80 registers, three CTAs per SM: alone the 64 x 64 / 4 x 4
+// tile is faster (1024 x 1024 x 128: 0.133 vs 0.142 ms), but beside the leaf chain the solve is (4.37 -> 4.21 ms)
+template <> struct GemmTile<2, 0> : Tile<64, 32, 16, 4, 2, 3> {};
 template <> struct GemmTile<2, 1> : Tile<32, 32, 16, 2, 2> {};
 template <> struct GemmTile<2, 2> : Tile<16, 64, 16, 1, 4> {};
 template <> struct GemmTile<2, 3> : Tile<64, 16, 16, 4, 1> {};
