@@ -268,17 +268,19 @@ def run_ours(args, ws, rank, local):
         ms = [a.elapsed_time(bb) for a, bb in ev]
         ms_step = max_over_ranks(sum(ms) / steps)
         out = {"ms_per_step": ms_step, "ms_min": min(ms), "launches_per_step": per_step_launches}
-        if with_e2e:  # through the public API from pinned host buffers, copies inside the timed region
+        if with_e2e:  # through the public API from pinned host buffers (mdls_lstsq_host plan), copies timed
             A_p = torch.from_numpy(A_h).pin_memory()
             b_p = torch.from_numpy(b_h).pin_memory()
             x_p = torch.empty((A_h.shape[0], K), dtype=torch.float64).pin_memory()
             if plan is None:
                 A_d, b_d = torch.empty_like(A), torch.empty_like(b)
+            else:  # mdls_lstsq_host_plan: the copies are inside the library graph, A's panels overlap the QR
+                hplan = mdls.HostLstsqPlan(prec, M, K, nb, form_q=True, device=dev, A=A_p, b=b_p, x=x_p)
 
             def e2e_step():
                 if plan is not None:
-                    x_p.copy_(plan.solve(A_p, b_p), non_blocking=True)
-                    return plan.info
+                    hplan.run()
+                    return hplan.info
                 A_d.copy_(A_p, non_blocking=True)
                 b_d.copy_(b_p, non_blocking=True)
                 rr = mdls.lstsq(prec, A_d, b_d, nb, form_q=True, work=work)

@@ -202,6 +202,21 @@ int mdls_trace_collect(double *stage_ms, double *family_ms, int64_t *family_laun
                              int64_t psa, int64_t strideA, const double *b, int64_t psb, int64_t strideB,          \
                              double *x, int64_t psx, int64_t strideX, int form_q, int groups, void *work,          \
                              size_t work_bytes, int *dev_info, void *stream);                                      \
+  /* least squares with HOST inputs and output (the end-to-end call): A (M x K, lda >= M, planes psa  \
+   * apart), b (planes psb >= M apart) and x (planes psx >= K apart) are in page-locked host memory (cudaHostAlloc \
+   * / torch pin_memory; pageable memory makes the copies synchronous).  b is copied first; A column panel by     \
+   * column panel (nb columns, every limb plane) on a library copy stream, one event per panel, so the leaf       \
+   * chain starts on panel 0 while the rest of A is in flight and every lane waits only for the panels it        \
+   * touches; x is copied back at the end.  Everything is stream-ordered on `stream` (x is valid after it        \
+   * synchronises).  work: mdls_workspace_<p>(form_q ? MDLS_OP_LSTSQ : MDLS_OP_LSTSQ_NOQ, M, K, nb) bytes (device). \
+   * Errors: -1..-3 sizes, -4 A, -7 b, -9 x, -13 workspace; dev_info as mdls_lstsq. */                          \
+  int mdls_lstsq_host_##P(int64_t M, int64_t K, int64_t nb, const double *A, int64_t lda, int64_t psa,            \
+                          const double *b, int64_t psb, double *x, int64_t psx, int form_q, void *work,           \
+                          size_t work_bytes, int *dev_info, void *stream);                                        \
+  /* plan version of mdls_lstsq_host_<p>: the host buffers are fixed at capture (keep them pinned and alive). */ \
+  int mdls_lstsq_host_plan_##P(int64_t M, int64_t K, int64_t nb, const double *A, int64_t lda, int64_t psa,       \
+                               const double *b, int64_t psb, double *x, int64_t psx, int form_q, void *work,      \
+                               size_t work_bytes, int *dev_info, void **plan);                                    \
   /* plan versions of mdls_lstsq_<p> and mdls_lstsq_batched_<p> (see "Plans" above); *plan = NULL on error. */  \
   int mdls_lstsq_plan_##P(int64_t M, int64_t K, int64_t nb, const double *A, int64_t lda, int64_t psa,            \
                           const double *b, int64_t psb, double *x, int64_t psx, int form_q, void *work,             \

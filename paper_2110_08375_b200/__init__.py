@@ -20,7 +20,7 @@ OPS = {"add": 0, "sub": 1, "mul": 2, "div": 3, "sqrt": 4, "sqrt_fast": 5, "recip
        "wrecip_fast": 9}
 T1_SUMS = {"dd": (20, 23, 70), "qd": (89, 336, 893), "od": (269, 1742, 5126), "d": (1, 1, 1)}  # P:102-136 (add, mul, div)
 
-__all__ = ["md_op", "qr", "apply_qt", "qt_b", "invert_tiles", "backsub", "lstsq", "norm2", "counts",
+__all__ = ["md_op", "qr", "apply_qt", "qt_b", "invert_tiles", "backsub", "lstsq", "lstsq_host", "norm2", "counts",
            "workspace_bytes", "PRECISIONS"]
 
 
@@ -345,6 +345,68 @@ class LstsqPlan(_Plan):
             self.b.copy_(b, non_blocking=True)
         self.run()
         return self.x
+
+
+class HostLstsqPlan(_Plan):
+    """Least squares from and to page-locked HOST memory as a replayable plan (mdls_lstsq_host_plan_<p>): pinned
+    host buffers A (m, K, M), b (m, M), x (m, K) -- the caller's (captured by address) or the plan's own -- plus the
+    device workspace and info.  run() replays the captured call: b and then A's column panels cross PCIe while the
+    factorisation of the first panels runs, x comes back at the end.  solve(A, b) first writes new inputs into the
+    pinned buffers (host copies), replays and returns the pinned x after synchronising the current stream."""
+
+    def __init__(self, prec: str, M: int, K: int, nb: int, form_q: bool = True, device=None, A=None, b=None, x=None):
+        torch = _torch()
+        dev = torch.device("cuda") if device is None else torch.device(device)
+        m = PRECISIONS[prec]
+        self.prec, self.M, self.K, self.nb = prec, M, K, nb
+
+        def pinned(t, shape, name):  # the caller's pinned buffer (captured by address) or a new one
+            if t is None:
+                return torch.zeros(shape, dtype=torch.float64).pin_memory()
+            if t.is_cuda or not t.is_pinned() or t.dtype != torch.float64 or tuple(t.shape) != shape \
+                    or not t.is_contiguous():
+                raise ValueError(f"HostLstsqPlan: {name} must be a pinned contiguous float64 host tensor {shape}")
+            return t
+        self.A = pinned(A, (m, K, M), "A")
+        self.b = pinned(b, (m, M), "b")
+        self.x = pinned(x, (m, K), "x")
+        self.info = torch.zeros(1, dtype=torch.int32, device=dev)
+        op = _lib.OP_LSTSQ if form_q else _lib.OP_LSTSQ_NOQ
+        self.work, nbytes = _work(prec, op, M, K, nb, dev)
+        self._capture(_lib.fn("mdls_lstsq_host_plan_", prec),
+                      (M, K, nb, _ptr(self.A), M, K * M, _ptr(self.b), M, _ptr(self.x), K, int(form_q),
+                       _ptr(self.work), nbytes, _ptr(self.info)))
+
+    def solve(self, A=None, b=None):
+        torch = _torch()
+        if A is not None:
+            self.A.copy_(torch.as_tensor(A))
+        if b is not None:
+            self.b.copy_(torch.as_tensor(b))
+        self.run()
+        torch.cuda.current_stream().synchronize()
+        return self.x
+
+
+def lstsq_host(prec: str, A, b, nb: int, form_q: bool = True):
+    """Least squares from pinned host tensors A (m, K, M) and b (m, M) (mdls_lstsq_host_<p>): returns (x, info),
+    x a pinned host (m, K) tensor, valid after the current stream synchronises (done here)."""
+    torch = _torch()
+    m = PRECISIONS[prec]
+    if A.is_cuda or b.is_cuda or not A.is_pinned() or not b.is_pinned():
+        raise ValueError("lstsq_host: A and b must be page-locked host tensors (tensor.pin_memory())")
+    if A.dtype != torch.float64 or A.dim() != 3 or A.shape[0] != m or not A.is_contiguous():
+        raise ValueError(f"lstsq_host: A must be contiguous float64 (m={m}, K, M)")
+    _, K, M = A.shape
+    x = torch.empty((m, K), dtype=torch.float64).pin_memory()
+    dev = torch.device("cuda")
+    work, nbytes = _work(prec, _lib.OP_LSTSQ if form_q else _lib.OP_LSTSQ_NOQ, M, K, nb, dev)
+    info = _info(dev)
+    rc = _lib.fn("mdls_lstsq_host_", prec)(M, K, nb, _ptr(A), M, K * M, _ptr(b), b.shape[1], _ptr(x), K, int(form_q),
+                                           _ptr(work), nbytes, _ptr(info), _stream())
+    _lib.check(rc, "lstsq_host")
+    torch.cuda.current_stream().synchronize()
+    return x, info
 
 
 class BatchedLstsqPlan(_Plan):

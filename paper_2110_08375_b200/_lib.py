@@ -53,6 +53,8 @@ _SIGS = {
     "mdls_workspace_batched_": (_Z, [_I, _L, _L, _L, _I]),
     "mdls_zlstsq_": (_I, [_L, _L, _L, _P, _P, _L, _L, _P, _P, _L, _P, _P, _L, _I, _P, _Z, _P, _P]),
     "mdls_lstsq_plan_": (_I, [_L, _L, _L, _P, _L, _L, _P, _L, _P, _L, _I, _P, _Z, _P, ctypes.POINTER(_P)]),
+    "mdls_lstsq_host_": (_I, [_L, _L, _L, _P, _L, _L, _P, _L, _P, _L, _I, _P, _Z, _P, _P]),
+    "mdls_lstsq_host_plan_": (_I, [_L, _L, _L, _P, _L, _L, _P, _L, _P, _L, _I, _P, _Z, _P, ctypes.POINTER(_P)]),
     "mdls_lstsq_batched_plan_": (_I, [_L, _L, _L, _L, _P, _L, _L, _L, _P, _L, _L, _P, _L, _L, _I, _I, _P, _Z, _P,
                                       ctypes.POINTER(_P)]),
     "mdls_qr_panel_": (_I, [_L, _L, _L, _P, _L, _L, _P, _L, _L, _P, _L, _L, _P, _Z, _P, _P]),

@@ -167,36 +167,84 @@ static QrBufs<M> qr_bufs(void* work, const Plan& p, int64_t Mr, int64_t K, int64
   return b;
 }
 
-// the whole least-squares pipeline of one problem on stream st (arguments already checked)
+// host-resident inputs / output of mdls_lstsq_host_<p> (pinned, limb-planar)
+struct HostIO {
+  const double* A;
+  int64_t lda, psa;
+  const double* b;
+  int64_t psb;
+  double* x;
+  int64_t psx;
+};
+
+// the whole least-squares pipeline of one problem on stream st (arguments already checked).  With hio the
+// inputs come from host memory: b first, then A column panel by column panel on a copy stream (one event
+// per panel), so the leaf chain starts on panel 0 while the rest of A is still crossing PCIe, and x is copied
+// back at the end -- the host<->device transfers overlap the factorisation instead of preceding it.
 static int lstsq_run(cudaStream_t st, int64_t Mr, int64_t K, int64_t nb, const double* A, int64_t lda, int64_t psa,
                      const double* b, int64_t psb, double* x, int64_t psx, int form_q, double* R_out, int64_t ldr,
                      int64_t psr, double* Q_out, int64_t ldq, int64_t psq, double* y_out, int64_t psy, void* work,
-                     int* dev_info) {
+                     int* dev_info, const HostIO* hio = nullptr) {
   const int op = form_q ? MDLS_OP_LSTSQ : MDLS_OP_LSTSQ_NOQ;
   const Plan p = make_plan<M>(op, Mr, K, nb);
   set_stage(MDLS_NSTAGES);
   QrBufs<M> bb = qr_bufs(work, p, Mr, K, nb, nullptr, 0, 0);
   int* pre = bb.info_slot + 2;
+  auto fork = [](cudaStream_t from, cudaStream_t to) {
+    cudaEvent_t ev = pool_event();
+    cudaEventRecord(ev, from);
+    cudaStreamWaitEvent(to, ev, 0);
+  };
   MDLS_LAUNCH(F_MISC, st, info_init_kernel<<<1, 1, 0, st>>>(bb.info_slot));
   MDLS_LAUNCH(F_MISC, st, info_init_kernel<<<1, 1, 0, st>>>(bb.info_slot + 1));
   MDLS_LAUNCH(F_MISC, st, int_set_kernel<<<1, 1, 0, st>>>(pre, 0));
-  MDLS_LAUNCH(F_MISC, st, finite_check_kernel<M><<<grid_for(Mr * K, 256), 256, 0, st>>>(Mr, K, CMat{A, lda, psa}, pre));
-  MDLS_LAUNCH(F_MISC, st, finite_check_kernel<M><<<grid_for(Mr, 256), 256, 0, st>>>(Mr, 1, CMat{b, Mr, psb}, pre));
   // factor a copy of A
   Mat Af{at<double>(work, p.af), Mr, Mr * K};
-  MDLS_LAUNCH(F_MISC, st, copy_kernel<M><<<grid_for(Mr * K, 256), 256, 0, st>>>(Mr, K, CMat{A, lda, psa}, Af, 0));
+  const int64_t NP = cdiv(K, nb);
+  std::vector<cudaEvent_t> ready;
+  cudaStream_t cs = nullptr;
+  if (hio) {
+    double* bdev = at<double>(work, p.v2);
+    for (int l = 0; l < M; ++l)
+      cudaMemcpyAsync(bdev + l * Mr, hio->b + l * hio->psb, sizeof(double) * Mr, cudaMemcpyHostToDevice, st);
+    b = bdev;
+    psb = Mr;
+    x = at<double>(work, p.hx);
+    psx = K;
+    cs = side_stream(7);
+    fork(st, cs);  // the previous call's use of Af is over
+    ready.resize((size_t)NP);
+    for (int64_t t = 0; t < NP; ++t) {
+      const int64_t c0 = t * nb, nc = std::min<int64_t>(K, c0 + nb) - c0;
+      for (int l = 0; l < M; ++l)
+        cudaMemcpy2DAsync(Af.p + l * Af.ps + c0 * Mr, sizeof(double) * Mr, hio->A + l * hio->psa + c0 * hio->lda,
+                          sizeof(double) * hio->lda, sizeof(double) * Mr, nc, cudaMemcpyHostToDevice, cs);
+      ready[(size_t)t] = pool_event();
+      cudaEventRecord(ready[(size_t)t], cs);
+    }
+    MDLS_LAUNCH(F_MISC, cs, finite_check_kernel<M><<<grid_for(Mr * K, 256), 256, 0, cs>>>(Mr, K, cm(Af), pre));
+  } else {
+    MDLS_LAUNCH(F_MISC, st, finite_check_kernel<M><<<grid_for(Mr * K, 256), 256, 0, st>>>(Mr, K, CMat{A, lda, psa}, pre));
+    MDLS_LAUNCH(F_MISC, st, copy_kernel<M><<<grid_for(Mr * K, 256), 256, 0, st>>>(Mr, K, CMat{A, lda, psa}, Af, 0));
+  }
+  MDLS_LAUNCH(F_MISC, st, finite_check_kernel<M><<<grid_for(Mr, 256), 256, 0, st>>>(Mr, 1, CMat{b, Mr, psb}, pre));
   cudaMemsetAsync(bb.Y.p, 0, sizeof(double) * M * Mr * K, st);
   cudaMemsetAsync(bb.W.p, 0, sizeof(double) * M * Mr * K, st);
   Mat Q = (form_q && Q_out) ? Mat{Q_out, ldq, psq} : Mat{form_q ? at<double>(work, p.q) : nullptr, Mr, Mr * Mr};
   const bool fwd = form_q && q_forward<M>();
   if (use_chain<M>(Mr, K, nb)) {
     if (qr_factor_chain<M>(st, Mr, K, nb, Af, bb, Mat{at<double>(work, p.t), 32, 32 * std::max<int64_t>(K, 32)},
-                           fwd ? &Q : nullptr) != cudaSuccess)
+                           fwd ? &Q : nullptr, hio ? ready.data() : nullptr) != cudaSuccess) {
+      if (cs) fork(cs, st);
       return MDLS_ERR_CUDA;
-  } else if (qr_factor_overlap<M>(bb.lane(0, st), bb.lane(1, side_stream(0)), bb.lane(2, side_stream(1)), Mr, K, nb,
-                                  Af, bb, fwd ? &Q : nullptr) != cudaSuccess) {
-    return MDLS_ERR_CUDA;
+    }
+  } else {
+    if (cs) fork(cs, st);  // the GEMM-chained path takes A whole
+    if (qr_factor_overlap<M>(bb.lane(0, st), bb.lane(1, side_stream(0)), bb.lane(2, side_stream(1)), Mr, K, nb, Af,
+                             bb, fwd ? &Q : nullptr) != cudaSuccess)
+      return MDLS_ERR_CUDA;
   }
+  if (cs) fork(cs, st);  // the copies and A's finite check are done before the info is read
   double* yv = at<double>(work, p.v1);
   if (form_q) {
     if (!fwd) form_q_backward<M>(st, Mr, K, nb, Q, bb);
@@ -212,6 +260,9 @@ static int lstsq_run(cudaStream_t st, int64_t Mr, int64_t K, int64_t nb, const d
   if (R_out) MDLS_LAUNCH(F_MISC, st, copy_kernel<M><<<grid_for(Mr * K, 256), 256, 0, st>>>(Mr, K, cm(Af), Mat{R_out, ldr, psr}, 1));
   if (y_out) MDLS_LAUNCH(F_MISC, st, copy_kernel<M><<<grid_for(Mr, 256), 256, 0, st>>>(Mr, 1, CMat{yv, Mr, Mr}, Mat{y_out, Mr, psy}, 0));
   if (dev_info) MDLS_LAUNCH(F_MISC, st, info_finish_kernel<<<1, 1, 0, st>>>(bb.info_slot, pre, dev_info));
+  if (hio)
+    for (int l = 0; l < M; ++l)
+      cudaMemcpyAsync(hio->x + l * hio->psx, x + l * psx, sizeof(double) * K, cudaMemcpyDeviceToHost, st);
   return launched();
 }
 
@@ -456,6 +507,44 @@ int MDLS_FN(mdls_lstsq_plan_)(int64_t Mr, int64_t K, int64_t nb, const double* A
   const int64_t n0 = mdls_launch_count();
   const int rc = lstsq_run(cs, Mr, K, nb, A, lda, psa, b, psb, x, psx, form_q, nullptr, 0, 0, nullptr, 0, 0, nullptr,
                            0, work, dev_info);
+  const int rc2 = capture_end(cs, mdls_launch_count() - n0, plan);
+  return rc ? rc : rc2;
+}
+
+// host-input least squares: A, b, x in pinned host memory (see include/mdls.h)
+static int lstsq_host_check(int64_t Mr, int64_t K, int64_t nb, const double* A, int64_t lda, int64_t psa,
+                            const double* b, int64_t psb, const double* x, int64_t psx, int form_q, const void* work,
+                            size_t work_bytes) {
+  if (int e = tile_ok(Mr, K, nb)) return e;
+  if (!mat_ok(A, Mr, K, lda, psa)) return -4;
+  if (!b || psb < Mr) return -7;
+  if (!x || psx < K) return -9;
+  const int op = form_q ? MDLS_OP_LSTSQ : MDLS_OP_LSTSQ_NOQ;
+  if (!work || work_bytes < make_plan<M>(op, Mr, K, nb).total) return -13;
+  return 0;
+}
+
+int MDLS_FN(mdls_lstsq_host_)(int64_t Mr, int64_t K, int64_t nb, const double* A, int64_t lda, int64_t psa,
+                              const double* b, int64_t psb, double* x, int64_t psx, int form_q, void* work,
+                              size_t work_bytes, int* dev_info, void* stream) {
+  if (int e = lstsq_host_check(Mr, K, nb, A, lda, psa, b, psb, x, psx, form_q, work, work_bytes)) return e;
+  const HostIO hio{A, lda, psa, b, psb, x, psx};
+  return lstsq_run(S(stream), Mr, K, nb, nullptr, 0, 0, nullptr, 0, nullptr, 0, form_q, nullptr, 0, 0, nullptr, 0, 0,
+                   nullptr, 0, work, dev_info, &hio);
+}
+
+int MDLS_FN(mdls_lstsq_host_plan_)(int64_t Mr, int64_t K, int64_t nb, const double* A, int64_t lda, int64_t psa,
+                                   const double* b, int64_t psb, double* x, int64_t psx, int form_q, void* work,
+                                   size_t work_bytes, int* dev_info, void** plan) {
+  if (!plan) return -15;
+  *plan = nullptr;
+  if (int e = lstsq_host_check(Mr, K, nb, A, lda, psa, b, psb, x, psx, form_q, work, work_bytes)) return e;
+  cudaStream_t cs = capture_begin();
+  if (!cs) return MDLS_ERR_CUDA;
+  const int64_t n0 = mdls_launch_count();
+  const HostIO hio{A, lda, psa, b, psb, x, psx};
+  const int rc = lstsq_run(cs, Mr, K, nb, nullptr, 0, 0, nullptr, 0, nullptr, 0, form_q, nullptr, 0, 0, nullptr, 0, 0,
+                           nullptr, 0, work, dev_info, &hio);
   const int rc2 = capture_end(cs, mdls_launch_count() - n0, plan);
   return rc ? rc : rc2;
 }

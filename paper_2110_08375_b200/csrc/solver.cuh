@@ -25,7 +25,7 @@ namespace mdls {
 // ---------------------------------------------------------------------------
 struct Plan {
   size_t af = 0, q = 0, y = 0, w = 0, beta = 0, s = 0, t = 0, x = 0, part = 0, v0 = 0, v1 = 0, v2 = 0, vt = 0, us = 0,
-         flags = 0, info = 0, total = 0;
+         flags = 0, hx = 0, info = 0, total = 0;
 };
 
 // md elements of one lane's split-K / stream-K partial buffer: kMaxSplit nb x max(M, K) partials, or the
@@ -47,7 +47,10 @@ Plan make_plan(int op, int64_t Mr, int64_t K, int64_t nb) {
   };
   const int64_t mx = std::max(Mr, K);
   const bool qr_like = (op == MDLS_OP_QR || op == MDLS_OP_LSTSQ || op == MDLS_OP_LSTSQ_NOQ);
-  if (op == MDLS_OP_LSTSQ || op == MDLS_OP_LSTSQ_NOQ) p.af = take(md * Mr * K);
+  if (op == MDLS_OP_LSTSQ || op == MDLS_OP_LSTSQ_NOQ) {
+    p.af = take(md * Mr * K);
+    p.hx = take(md * K);  // device x of a host-input solve (mdls_lstsq_host)
+  }
   if (op == MDLS_OP_LSTSQ) p.q = take(md * Mr * Mr);
   if (qr_like) {
     p.y = take(md * Mr * K);
@@ -259,7 +262,7 @@ bool chain_supported(int64_t Mr, int64_t K, int64_t nb) {
 
 template <int M>
 cudaError_t qr_factor_chain(cudaStream_t st, int64_t Mr, int64_t K, int64_t nb, Mat A, const QrBufs<M>& b, Mat Tall,
-                            Mat* Qf) {
+                            Mat* Qf, const cudaEvent_t* panel_ready = nullptr) {
   auto fork = [](cudaStream_t from, cudaStream_t to) {
     cudaEvent_t ev = pool_event();
     cudaEventRecord(ev, from);
@@ -269,6 +272,17 @@ cudaError_t qr_factor_chain(cudaStream_t st, int64_t Mr, int64_t K, int64_t nb, 
                Lbs = side_stream(4), Lfs = side_stream(5);
   const Lane La = b.lane(0, Las), Lw = b.lane(1, Lws), Lq = b.lane(2, Lqs), Lb = b.lane(3, Lbs), Lf = b.lane(4, Lfs);
   for (cudaStream_t q : {Lc, Las, Lws, Lqs, Lbs, Lfs}) fork(st, q);
+  // host-input solves (mdls_lstsq_host): column panel p of A arrives by its own copy, recorded in panel_ready[p];
+  // each lane waits for the panels it is about to touch, once (the leaf chain for its panel, the near window up
+  // to its last column, the far window for panel k+2, the panel products for all of A)
+  const int64_t NP = cdiv(K, nb);
+  std::vector<int64_t> panels_seen(8, -1);
+  auto need = [&](int lane_id, cudaStream_t q, int64_t last_col) {
+    if (!panel_ready || last_col < 0) return;
+    const int64_t pidx = std::min<int64_t>(NP - 1, last_col / nb);
+    for (int64_t t = panels_seen[(size_t)lane_id] + 1; t <= pidx; ++t) cudaStreamWaitEvent(q, panel_ready[t], 0);
+    panels_seen[(size_t)lane_id] = std::max(panels_seen[(size_t)lane_id], pidx);
+  };
   if (Qf) {
     set_stage(MDLS_ST_FORM_Q);
     MDLS_LAUNCH(F_MISC, Lqs, set_identity_kernel<M><<<grid_for(Mr * Mr, 256), 256, 0, Lqs>>>(Mr, Mr, *Qf));
@@ -342,6 +356,7 @@ cudaError_t qr_factor_chain(cudaStream_t st, int64_t Mr, int64_t K, int64_t nb, 
     if (timeline) tl_ls.push_back(tl_ev(Lc));
     set_stage(MDLS_ST_PANEL);
     const Mat Tp = s > 0 ? Mat{Tall.p + jss[(size_t)s - 1] * 32, 32, Tall.ps} : Mat{nullptr, 0, 0};
+    need(0, Lc, js + B - 1);
     err = launch_leaf_chain<M>(Lc, Mr, js, B, A, b.Y, b.beta, K, Ts, b.info_slot, Tp, s > 0 ? jss[(size_t)s - 1] : -1);
     if (err != cudaSuccess) break;
     cudaEventRecord(ev_leaf, Lc);
@@ -352,6 +367,7 @@ cudaError_t qr_factor_chain(cudaStream_t st, int64_t Mr, int64_t K, int64_t nb, 
     cudaStreamWaitEvent(Las, ev_leaf, 0);
     if (defer && first_in_panel && k >= 1 && ev_far[(size_t)k - 1]) cudaStreamWaitEvent(Las, ev_far[(size_t)k - 1], 0);
     const int64_t c1 = defer ? std::min<int64_t>(K, (k + 2) * nb) : K;
+    if (c0 < c1) need(1, Las, c1 - 1);
     leaf_update(La, s, c0, c1);
     ev_apply[(size_t)s] = pool_event();
     cudaEventRecord(ev_apply[(size_t)s], Las);
@@ -360,6 +376,7 @@ cudaError_t qr_factor_chain(cudaStream_t st, int64_t Mr, int64_t K, int64_t nb, 
     if (defer && (k + 2) * nb < K) {
       cudaStreamWaitEvent(Lfs, ev_leaf, 0);
       if (first_in_panel && k >= 1 && ev_bulk_a[(size_t)k - 1]) cudaStreamWaitEvent(Lfs, ev_bulk_a[(size_t)k - 1], 0);
+      need(5, Lfs, std::min<int64_t>(K, (k + 3) * nb) - 1);
       leaf_update(Lf, s, std::max<int64_t>(c0, (k + 2) * nb), std::min<int64_t>(K, (k + 3) * nb));
     }
     if (defer && last_in_panel) {
@@ -381,6 +398,7 @@ cudaError_t qr_factor_chain(cudaStream_t st, int64_t Mr, int64_t K, int64_t nb, 
       const int64_t cb = (k + 3) * nb;
       if (defer && cb < K) {
         fork(Lws, Lbs);
+        need(4, Lbs, K - 1);
         GemmCap cap(bcap);
         const int64_t cm1 = std::min<int64_t>(K, cb + nb);
         qr_apply_panel<M>(Lb, Mr, nb, k, Yk, Wk, A, cb, cm1);

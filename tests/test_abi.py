@@ -79,6 +79,17 @@ def test_host_argument_checks(prec):
     assert _lib.fn("mdls_lstsq_batched_plan_", prec)(*bad) == -16
     assert _lib.load().mdls_plan_launch(nul, nul) == -1
     _lib.load().mdls_plan_destroy(nul)
+    host = _lib.fn("mdls_lstsq_host_", prec)
+    assert host(10, 20, 4, fake, 10, 200, fake, 10, fake, 20, 1, fake, 1 << 30, nul, nul) == -1   # M < K
+    assert host(20, 8, 4, nul, 20, 160, fake, 20, fake, 8, 1, fake, 1 << 30, nul, nul) == -4     # NULL A
+    assert host(20, 8, 4, fake, 20, 160, fake, 10, fake, 8, 1, fake, 1 << 30, nul, nul) == -7    # psb < M
+    assert host(20, 8, 4, fake, 20, 160, fake, 20, fake, 4, 1, fake, 1 << 30, nul, nul) == -9    # psx < K
+    assert host(20, 8, 4, fake, 20, 160, fake, 20, fake, 8, 1, nul, 0, nul, nul) == -13         # no workspace
+    assert _lib.fn("mdls_lstsq_host_plan_", prec)(20, 8, 4, fake, 20, 160, fake, 20, fake, 8, 1, fake, 1 << 30, nul,
+                                                  None) == -15                                      # NULL plan
+    hp = ctypes.c_void_p(0)
+    assert _lib.fn("mdls_lstsq_host_plan_", prec)(10, 20, 4, fake, 10, 200, fake, 10, fake, 20, 1, fake, 1 << 30, nul,
+                                                  ctypes.byref(hp)) == -1 and hp.value is None
     assert _lib.fn("mdls_workspace_", prec)(0, 10, 20, 4) == 0
     assert _lib.fn("mdls_workspace_", prec)(2, 1024, 1024, 128) > 0
 
