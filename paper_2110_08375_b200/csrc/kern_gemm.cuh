@@ -374,32 +374,41 @@ void gemm(cudaStream_t st, int64_t m, int64_t n, int64_t k, CMat A, CMat B, Mat 
 // merges, fixed order) and multiplied by -T^T (T: B x B upper, ld 32) in one
 // kernel; a CTA = 16 columns x B rows.  X then feeds C += Y X.
 // ---------------------------------------------------------------------------
-template <int M, int B>
-__global__ void __launch_bounds__(16 * B) splitk_reduce_t_kernel(int64_t n, int64_t S, const double* __restrict__ part,
-                                                                 CMat T, double* X, int64_t ldx, int64_t psx) {
+template <int M, int B, int ZG>
+__global__ void __launch_bounds__(16 * B * ZG) splitk_reduce_t_kernel(int64_t n, int64_t S, const double* __restrict__ part,
+                                                                      CMat T, double* X, int64_t ldx, int64_t psx) {
+  // ZG thread groups split the S partials (group g sums z = g, g + ZG, ...: S / ZG dependent merges instead of S),
+  // then group 0 merges the ZG sums in group order (fixed: bitwise reproducible)
+  __shared__ Acc<M> Zp[ZG][16][B];
   __shared__ md<M> Z[16][B];
-  const int p = threadIdx.x % B, jl = threadIdx.x / B;
+  const int p = threadIdx.x % B, jl = (threadIdx.x / B) % 16, zg = threadIdx.x / (16 * B);
   const int64_t j = (int64_t)blockIdx.x * 16 + jl;
   const int64_t pps = (int64_t)B * n * S;
+  Acc<M> acc;
+  acc.init();
   if (j < n) {
-    Acc<M> acc;
-    acc.init();
 #pragma unroll 4
-    for (int64_t z = 0; z < S; ++z) {  // unrolled: the partial loads are issued ahead of the merges
+    for (int64_t z = zg; z < S; z += ZG) {  // unrolled: the partial loads are issued ahead of the merges
       const md<M> pz = ld<M>(part, pps, p + (j + z * n) * B);
       Acc<M> o;
 #pragma unroll
       for (int k = 0; k < Acc<M>::NV; ++k) o.r(k) = (k < M) ? pz.v[k] : 0.0;
       acc.merge(o);
     }
+  }
+  Zp[zg][jl][p] = acc;
+  __syncthreads();
+  if (zg == 0 && j < n) {
+#pragma unroll
+    for (int g = 1; g < ZG; ++g) acc.merge(Zp[g][jl][p]);
     Z[jl][p] = acc.get();
   }
   __syncthreads();
-  if (j < n) {
-    Acc<M> acc;
-    acc.init();
-    for (int q = 0; q <= p; ++q) acc.add_prod(ld<M>(T.p, T.ps, q + (int64_t)p * T.ld), Z[jl][q]);
-    st<M>(X, psx, p + j * ldx, neg(acc.get()));
+  if (zg == 0 && j < n) {
+    Acc<M> a2;
+    a2.init();
+    for (int q = 0; q <= p; ++q) a2.add_prod(ld<M>(T.p, T.ps, q + (int64_t)p * T.ld), Z[jl][q]);
+    st<M>(X, psx, p + j * ldx, neg(a2.get()));
   }
 }
 
@@ -417,10 +426,12 @@ void leaf_t_product(cudaStream_t st, int B, int64_t n, int64_t r, CMat Y, CMat T
   S = std::max<int64_t>(1, cdiv(r, kc));
   GemmArgs g{B, n, r, Y.p, Y.ld, Y.ps, C.p, C.ld, C.ps, nullptr, B, 0, 0, kc, part, S};
   gemm_kernel_launch<M, 2, true, false>(st, g);
+  // z-groups per output: 4 (2 for od: registers and static shared memory); od leaves are 8 wide
+  constexpr int ZG8 = (M == 8) ? 2 : 4, ZG16 = (M == 8) ? 1 : 4;
   if (B == 16)
-    MDLS_LAUNCH(F_GEMM, st, splitk_reduce_t_kernel<M, 16><<<(unsigned)cdiv(n, 16), 256, 0, st>>>(n, S, part, T, X.p, X.ld, X.ps));
+    MDLS_LAUNCH(F_GEMM, st, splitk_reduce_t_kernel<M, 16, ZG16><<<(unsigned)cdiv(n, 16), 16 * 16 * ZG16, 0, st>>>(n, S, part, T, X.p, X.ld, X.ps));
   else
-    MDLS_LAUNCH(F_GEMM, st, splitk_reduce_t_kernel<M, 8><<<(unsigned)cdiv(n, 16), 128, 0, st>>>(n, S, part, T, X.p, X.ld, X.ps));
+    MDLS_LAUNCH(F_GEMM, st, splitk_reduce_t_kernel<M, 8, ZG8><<<(unsigned)cdiv(n, 16), 16 * 8 * ZG8, 0, st>>>(n, S, part, T, X.p, X.ld, X.ps));
 }
 
 
