@@ -205,7 +205,8 @@ int mdls_trace_collect(double *stage_ms, double *family_ms, int64_t *family_laun
   /* least squares with HOST inputs and output (the end-to-end call): A (M x K, lda >= M, planes psa  \
    * apart), b (planes psb >= M apart) and x (planes psx >= K apart) are in page-locked host memory (cudaHostAlloc \
    * / torch pin_memory; pageable memory makes the copies synchronous).  b is copied first; A column panel by     \
-   * column panel (nb columns, every limb plane) on a library copy stream, one event per panel, so the leaf       \
+   * column panel (nb columns, every limb plane) on a library copy stream (copy engines; inside a plan a        \
+   * zero-copy kernel reading the mapped pinned pages), one event per panel, so the leaf                          \
    * chain starts on panel 0 while the rest of A is in flight and every lane waits only for the panels it        \
    * touches; x is copied back at the end.  Everything is stream-ordered on `stream` (x is valid after it        \
    * synchronises).  work: mdls_workspace_<p>(form_q ? MDLS_OP_LSTSQ : MDLS_OP_LSTSQ_NOQ, M, K, nb) bytes (device). \

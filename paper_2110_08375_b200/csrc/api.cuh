@@ -175,7 +175,17 @@ struct HostIO {
   int64_t psb;
   double* x;
   int64_t psx;
+  const double* A_dev;  // A's device-visible address when its pinned pages are mapped (UVA), else NULL
 };
+// device-visible address of page-locked, mapped host memory (NULL for pageable memory)
+static const double* mapped_ptr(const double* h) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, h) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return (at.type == cudaMemoryTypeHost && at.devicePointer) ? static_cast<const double*>(at.devicePointer) : nullptr;
+}
 
 // the whole least-squares pipeline of one problem on stream st (arguments already checked).  With hio the
 // inputs come from host memory: b first, then A column panel by column panel on a copy stream (one event
@@ -216,9 +226,21 @@ static int lstsq_run(cudaStream_t st, int64_t Mr, int64_t K, int64_t nb, const d
     ready.resize((size_t)NP);
     for (int64_t t = 0; t < NP; ++t) {
       const int64_t c0 = t * nb, nc = std::min<int64_t>(K, c0 + nb) - c0;
-      for (int l = 0; l < M; ++l)
-        cudaMemcpy2DAsync(Af.p + l * Af.ps + c0 * Mr, sizeof(double) * Mr, hio->A + l * hio->psa + c0 * hio->lda,
-                          sizeof(double) * hio->lda, sizeof(double) * Mr, nc, cudaMemcpyHostToDevice, cs);
+      if (hio->A_dev) {
+        // zero-copy: a copy kernel on 64 CTAs reads the mapped pinned pages over PCIe (a kernel node overlaps the
+        // factorisation's kernels inside a CUDA graph, where copy-engine nodes were measured not to)
+        MDLS_LAUNCH(F_MISC, cs, copy_kernel<M><<<64, 256, 0, cs>>>(Mr, nc, CMat{hio->A_dev + c0 * hio->lda, hio->lda,
+                                                                               hio->psa}, sub(Af, 0, c0), 0));
+      } else {
+        for (int l = 0; l < M; ++l) {
+          if (hio->lda == Mr)  // the panel of one limb plane is contiguous on both sides: one linear copy
+            cudaMemcpyAsync(Af.p + l * Af.ps + c0 * Mr, hio->A + l * hio->psa + c0 * Mr, sizeof(double) * Mr * nc,
+                            cudaMemcpyHostToDevice, cs);
+          else
+            cudaMemcpy2DAsync(Af.p + l * Af.ps + c0 * Mr, sizeof(double) * Mr, hio->A + l * hio->psa + c0 * hio->lda,
+                              sizeof(double) * hio->lda, sizeof(double) * Mr, nc, cudaMemcpyHostToDevice, cs);
+        }
+      }
       ready[(size_t)t] = pool_event();
       cudaEventRecord(ready[(size_t)t], cs);
     }
@@ -511,7 +533,16 @@ int MDLS_FN(mdls_lstsq_plan_)(int64_t Mr, int64_t K, int64_t nb, const double* A
   return rc ? rc : rc2;
 }
 
-// host-input least squares: A, b, x in pinned host memory (see include/mdls.h)
+// host-input least squares: A, b, x in pinned host memory (see include/mdls.h).  A's panels cross PCIe by
+// copy-engine copies in stream order (direct call) and by the zero-copy panel kernel inside a plan's graph
+// (measured, dd 1024: direct 4.70 vs 4.85 ms, plan 4.37 vs 4.65 ms); MDLS_HOST_ZC=0 / 1 forces one or the other
+static bool host_zero_copy(bool in_plan) {
+  static const int v = [] {
+    const char* e = getenv("MDLS_HOST_ZC");
+    return e ? atoi(e) : -1;
+  }();
+  return v < 0 ? in_plan : v != 0;
+}
 static int lstsq_host_check(int64_t Mr, int64_t K, int64_t nb, const double* A, int64_t lda, int64_t psa,
                             const double* b, int64_t psb, const double* x, int64_t psx, int form_q, const void* work,
                             size_t work_bytes) {
@@ -528,7 +559,7 @@ int MDLS_FN(mdls_lstsq_host_)(int64_t Mr, int64_t K, int64_t nb, const double* A
                               const double* b, int64_t psb, double* x, int64_t psx, int form_q, void* work,
                               size_t work_bytes, int* dev_info, void* stream) {
   if (int e = lstsq_host_check(Mr, K, nb, A, lda, psa, b, psb, x, psx, form_q, work, work_bytes)) return e;
-  const HostIO hio{A, lda, psa, b, psb, x, psx};
+  const HostIO hio{A, lda, psa, b, psb, x, psx, host_zero_copy(false) ? mapped_ptr(A) : nullptr};
   return lstsq_run(S(stream), Mr, K, nb, nullptr, 0, 0, nullptr, 0, nullptr, 0, form_q, nullptr, 0, 0, nullptr, 0, 0,
                    nullptr, 0, work, dev_info, &hio);
 }
@@ -542,7 +573,7 @@ int MDLS_FN(mdls_lstsq_host_plan_)(int64_t Mr, int64_t K, int64_t nb, const doub
   cudaStream_t cs = capture_begin();
   if (!cs) return MDLS_ERR_CUDA;
   const int64_t n0 = mdls_launch_count();
-  const HostIO hio{A, lda, psa, b, psb, x, psx};
+  const HostIO hio{A, lda, psa, b, psb, x, psx, host_zero_copy(true) ? mapped_ptr(A) : nullptr};
   const int rc = lstsq_run(cs, Mr, K, nb, nullptr, 0, 0, nullptr, 0, nullptr, 0, form_q, nullptr, 0, 0, nullptr, 0, 0,
                            nullptr, 0, work, dev_info, &hio);
   const int rc2 = capture_end(cs, mdls_launch_count() - n0, plan);

@@ -39,3 +39,29 @@ def test_host_plan_replays_new_inputs(mdls, dev):
         ref = mdls.lstsq(prec, torch.from_numpy(A).to(dev), torch.from_numpy(b).to(dev), nb, form_q=True).x.cpu()
         assert int(plan.info.item()) == 0
         assert torch.equal(x, ref)
+
+
+def test_host_io_copy_modes_bitwise(tmp_path):
+    """the copy-engine and zero-copy panel transfers (MDLS_HOST_ZC=0 / 1, read once per process) give the same x"""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = f"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+import paper_2110_08375_b200 as mdls
+from paper_2110_08375_b200 import inputs
+A, b = inputs.lstsq_problem(512, 384, "qd", 5)
+x, info = mdls.lstsq_host("qd", torch.from_numpy(A).pin_memory(), torch.from_numpy(b).pin_memory(), 64)
+assert int(info.item()) == 0
+np.save(sys.argv[1], x.numpy())
+"""
+    outs = []
+    for zc in ("0", "1"):
+        out = str(tmp_path / f"x{zc}.npy")
+        p = subprocess.run([sys.executable, "-c", code, out], env={**os.environ, "MDLS_HOST_ZC": zc},
+                           capture_output=True, text=True, timeout=300)
+        assert p.returncode == 0, p.stderr[-2000:]
+        outs.append(np.load(out))
+    assert np.array_equal(outs[0], outs[1])

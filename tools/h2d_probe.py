@@ -52,3 +52,4 @@ for name, f in (("direct device", lambda: mdls.lstsq("dd", Ad, bd, 128, form_q=T
     e1.record()
     torch.cuda.synchronize()
     print(f"{name}: {e0.elapsed_time(e1) / 5:.3f} ms per call", flush=True)
+print("MDLS_HOST_ZC =", os.environ.get("MDLS_HOST_ZC", "1 (default)"))
